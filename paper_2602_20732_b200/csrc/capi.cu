@@ -1,0 +1,387 @@
+// capi.cu — extern "C" entry points of libchess_b200.so (include/chess_b200.h).
+//
+// Host-side validation mirrors the reference's error sites (config.py:36-48,
+// selection.py:55-56/68-72, hierarchy.py:108-114, kv_store.py:161-164); every
+// check happens before launch, no entry point synchronises its stream.
+#include <cstdarg>
+#include <mutex>
+
+#include "common.cuh"
+
+namespace chess {
+
+int launch_reset(const ChessState&, const uint8_t*, cudaStream_t);
+int launch_append(const ChessState&, const Workspace&, const void*, const void*, int64_t,
+                  const uint8_t*, cudaStream_t);
+int launch_seal(const ChessState&, const Workspace&, cudaStream_t);
+int launch_build(const ChessState&, const int32_t*, cudaStream_t);
+int launch_from_vectors(const ChessState&, int, const double*, int, int64_t, const int32_t*,
+                        cudaStream_t);
+int launch_mean_rows(const void*, int, int64_t, int64_t, int64_t, double*, cudaStream_t);
+int launch_select(const ChessState&, const Workspace&, const SelParams&, int, cudaStream_t);
+int launch_build_ws_all(const ChessState&, cudaStream_t);
+int launch_score_rows(const void*, int, int64_t, int64_t, int64_t, const double*, double*,
+                      cudaStream_t);
+int launch_prune(const double*, int, const double*, int, const double*, int, const int64_t*,
+                 const int64_t*, double, double, double, int32_t*, int32_t*, void*, cudaStream_t);
+int launch_topk(const double*, int, int, const uint8_t*, int32_t*, int32_t*, int, void*,
+                cudaStream_t);
+int launch_working_set(const int32_t*, int, int, int, int, const int32_t*, int32_t*, int8_t*,
+                       int32_t*, int32_t*, cudaStream_t);
+int launch_gather_pages(const int32_t*, int, const int64_t*, int, int32_t*, int32_t*,
+                        cudaStream_t);
+int launch_sparse_decode(const ChessState&, const Workspace&, int, const void*, int64_t, void*,
+                         int64_t, float*, float, cudaStream_t);
+int launch_entropy_trigger(const ChessState&, const Workspace&, const float*, int64_t, int64_t,
+                           const ChessTriggerCfg&, double*, cudaStream_t);
+int launch_entropy_logits(const Workspace&, const float*, int64_t, int64_t, int64_t, double*,
+                          cudaStream_t);
+int launch_entropy_probs(const double*, int64_t, int64_t, int64_t, double*, int32_t*,
+                         cudaStream_t);
+int launch_page_uncertainty(const double*, int, double*, cudaStream_t);
+int launch_fold(const ChessState&, const Workspace&, int, const void*, int, int, int64_t,
+                cudaStream_t);
+int launch_record_entropy(const ChessState&, const double*, const uint8_t*,
+                          const ChessTriggerCfg&, cudaStream_t);
+int attn_ctas_for(const ChessDims&);
+
+static thread_local char g_err[512] = {0};
+
+void set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+int fail(int code, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+  return code;
+}
+
+int check_launch(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(CHESS_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+  return CHESS_OK;
+}
+
+int num_sms() {
+  static int cached = 0;
+  if (cached == 0) {
+    int dev = 0, n = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess &&
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess && n > 0)
+      cached = n;
+    else {
+      cudaGetLastError();
+      cached = 148;
+    }
+  }
+  return cached;
+}
+
+static size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+size_t workspace_layout(const ChessDims& d, void* base, Workspace* ws) {
+  const int64_t b = d.batch;
+  const int64_t mr = max_rows(d);
+  const int64_t nsl = (d.ld + kScanSlice - 1) / kScanSlice;
+  const int64_t gq = d.kv_heads > 0 ? d.q_heads / d.kv_heads : 1;
+  const int64_t attn_slots = b * d.kv_heads + kAttnCtasMax;
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    const size_t o = off;
+    off = align_up(off + bytes, 256);
+    return o;
+  };
+  const size_t o_sel_done = take(b * 4);
+  const size_t o_cand = take(b * 3 * mr * 4);
+  const size_t o_cand_n = take(b * 4 * 4);
+  const size_t o_scores = take(b * mr * 8);
+  const size_t o_keys = take(b * mr * 8);
+  const size_t o_part = take(b * mr * nsl * 8);
+  const size_t o_kept = take(b * mr * 4);
+  const size_t o_plist = take(b * mr * 4);
+  const size_t o_attn_done = take(b * d.kv_heads * 4);
+  const size_t o_attn_part = take(attn_slots * gq * (d.head_dim + 2) * 4);
+  const size_t o_ent_done = take(b * 4);
+  const size_t o_ent_part = take(b * kEntSplit * 3 * 8);
+  const size_t o_app = take(b * 4);
+  const size_t o_seal = take(b * 4);
+  if (ws && base) {
+    uint8_t* p = reinterpret_cast<uint8_t*>(base);
+    ws->sel_done = reinterpret_cast<int32_t*>(p + o_sel_done);
+    ws->cand = reinterpret_cast<int32_t*>(p + o_cand);
+    ws->cand_n = reinterpret_cast<int32_t*>(p + o_cand_n);
+    ws->scores = reinterpret_cast<double*>(p + o_scores);
+    ws->keys = reinterpret_cast<uint64_t*>(p + o_keys);
+    ws->part = reinterpret_cast<double*>(p + o_part);
+    ws->kept = reinterpret_cast<int32_t*>(p + o_kept);
+    ws->plist = reinterpret_cast<int32_t*>(p + o_plist);
+    ws->attn_done = reinterpret_cast<int32_t*>(p + o_attn_done);
+    ws->attn_part = reinterpret_cast<float*>(p + o_attn_part);
+    ws->ent_done = reinterpret_cast<int32_t*>(p + o_ent_done);
+    ws->ent_part = reinterpret_cast<double*>(p + o_ent_part);
+    ws->append_done = reinterpret_cast<int32_t*>(p + o_app);
+    ws->seal_done = reinterpret_cast<int32_t*>(p + o_seal);
+    ws->n_slices = (int32_t)nsl;
+    ws->attn_ctas = std::min(attn_ctas_for(d), kAttnCtasMax);
+  }
+  return off;
+}
+
+static int validate(const ChessDims& d) {
+  if (d.batch < 1 || d.batch > kMaxBatch) return fail(CHESS_ERR_CONFIG, "batch must be in [1, %d]", kMaxBatch);
+  if (d.page_size < 1) return fail(CHESS_ERR_CONFIG, "page_size must be >= 1, got %d", d.page_size);
+  if (d.page_size > 256) return fail(CHESS_ERR_UNSUPPORTED, "page_size must be <= 256");
+  if (d.pages_per_chunk < 1 || d.chunks_per_grid < 1) return fail(CHESS_ERR_CONFIG, "hierarchy fan-outs must be >= 1");
+  if (d.window_pages < 1) return fail(CHESS_ERR_CONFIG, "window_pages must be >= 1");
+  if (d.layers < 1 || d.kv_heads < 1 || d.head_dim < 1 || d.q_heads < d.kv_heads || d.q_heads % d.kv_heads)
+    return fail(CHESS_ERR_CONFIG, "bad model shape");
+  if (d.dim != (int64_t)d.layers * d.kv_heads * d.head_dim)
+    return fail(CHESS_ERR_CONFIG, "dim must equal layers*kv_heads*head_dim");
+  if (d.ld < d.dim || d.ld % 4) return fail(CHESS_ERR_CONFIG, "ld must be >= dim and a multiple of 4");
+  if (d.max_pages < 1 || d.max_ws < 1) return fail(CHESS_ERR_CONFIG, "max_pages/max_ws must be >= 1");
+  if (d.n_phys < 1) return fail(CHESS_ERR_CONFIG, "store capacity must be >= 1 page");
+  if (d.summary_dtype != 0 && d.summary_dtype != 1) return fail(CHESS_ERR_CONFIG, "summary_dtype must be 0 or 1");
+  return CHESS_OK;
+}
+
+static int state_ws(const ChessState* st, Workspace* ws) {
+  if (!st) return fail(CHESS_ERR_CONFIG, "null state");
+  int rc = validate(st->d);
+  if (rc) return rc;
+  const size_t need = workspace_layout(st->d, nullptr, nullptr);
+  if (!st->workspace || st->workspace_bytes < need)
+    return fail(CHESS_ERR_CONFIG, "workspace too small: need %zu bytes", need);
+  workspace_layout(st->d, st->workspace, ws);
+  return CHESS_OK;
+}
+
+}  // namespace chess
+
+using namespace chess;
+
+extern "C" {
+
+int chess_abi_version(void) { return CHESS_ABI_VERSION; }
+size_t chess_dims_sizeof(void) { return sizeof(ChessDims); }
+size_t chess_state_sizeof(void) { return sizeof(ChessState); }
+
+int chess_last_error(char* buf, size_t n) {
+  if (buf && n) {
+    strncpy(buf, g_err, n - 1);
+    buf[n - 1] = 0;
+  }
+  return (int)strlen(g_err);
+}
+
+int chess_validate_dims(const ChessDims* d) {
+  if (!d) return fail(CHESS_ERR_CONFIG, "null dims");
+  return validate(*d);
+}
+
+size_t chess_workspace_bytes(const ChessDims* d) {
+  if (!d || validate(*d)) return 0;
+  return workspace_layout(*d, nullptr, nullptr);
+}
+
+int chess_reset_slots(const ChessState* st, const uint8_t* mask, void* stream) {
+  Workspace ws;
+  int rc = state_ws(st, &ws);
+  if (rc) return rc;
+  return launch_reset(*st, mask, (cudaStream_t)stream);
+}
+
+int chess_append_kv(const ChessState* st, const void* k_rows, const void* v_rows,
+                    int64_t row_stride, const uint8_t* active, void* stream) {
+  Workspace ws;
+  int rc = state_ws(st, &ws);
+  if (rc) return rc;
+  if (!k_rows || !v_rows || row_stride < st->d.dim) return fail(CHESS_ERR_SHAPE, "append: bad rows");
+  return launch_append(*st, ws, k_rows, v_rows, row_stride, active, (cudaStream_t)stream);
+}
+
+int chess_summary_seal(const ChessState* st, void* stream) {
+  Workspace ws;
+  int rc = state_ws(st, &ws);
+  if (rc) return rc;
+  return launch_seal(*st, ws, (cudaStream_t)stream);
+}
+
+int chess_summary_build(const ChessState* st, const int32_t* n_pages, void* stream) {
+  Workspace ws;
+  int rc = state_ws(st, &ws);
+  if (rc) return rc;
+  if (!n_pages) return fail(CHESS_ERR_CONFIG, "summary_build: null n_pages");
+  return launch_build(*st, n_pages, (cudaStream_t)stream);
+}
+
+int chess_summary_from_vectors(const ChessState* st, int32_t seq, const double* rows, int32_t n,
+                               int64_t row_stride, void* stream) {
+  Workspace ws;
+  int rc = state_ws(st, &ws);
+  if (rc) return rc;
+  if (seq < 0 || seq >= st->d.batch) return fail(CHESS_ERR_INDEX, "slot %d out of range", seq);
+  if (n < 0 || n > st->d.max_pages) return fail(CHESS_ERR_CONFIG, "from_vectors: %d rows exceed capacity", n);
+  if (n > 0 && (!rows || row_stride < st->d.dim)) return fail(CHESS_ERR_SHAPE, "from_vectors: bad rows");
+  // device copy of n for the epilogue: reuse the slot's sel_done counter cell? no —
+  // use the append counter of `seq` temporarily is unsafe; write into cand_n.
+  int32_t* n_dev = ws.cand_n + 4 * seq + 3;
+  cudaMemcpyAsync(n_dev, &n, sizeof(int32_t), cudaMemcpyHostToDevice, (cudaStream_t)stream);
+  return launch_from_vectors(*st, seq, rows, n, row_stride, n_dev, (cudaStream_t)stream);
+}
+
+int chess_summary_fold(const ChessState* st, int32_t seq, const void* rows, int32_t dtype,
+                       int32_t n_rows, int64_t row_stride, void* stream) {
+  Workspace ws;
+  int rc = state_ws(st, &ws);
+  if (rc) return rc;
+  if (seq < 0 || seq >= st->d.batch) return fail(CHESS_ERR_INDEX, "slot %d out of range", seq);
+  if (n_rows < 1) return fail(CHESS_ERR_ORDER, "only sealed pages can be finalized");
+  if (!rows || row_stride < st->d.dim) return fail(CHESS_ERR_SHAPE, "fold: bad rows");
+  if (dtype < 0 || dtype > 2) return fail(CHESS_ERR_CONFIG, "bad dtype");
+  return launch_fold(*st, ws, seq, rows, dtype, n_rows, row_stride, (cudaStream_t)stream);
+}
+
+int chess_record_entropy(const ChessState* st, const double* entropy, const uint8_t* active,
+                         const ChessTriggerCfg* cfg, void* stream) {
+  Workspace ws;
+  int rc = state_ws(st, &ws);
+  if (rc) return rc;
+  if (!cfg || !entropy) return fail(CHESS_ERR_CONFIG, "record_entropy: null argument");
+  if (cfg->policy < 0 || cfg->policy > 4) return fail(CHESS_ERR_CONFIG, "unknown policy %d", cfg->policy);
+  if (cfg->policy == CHESS_POLICY_FIXED && cfg->interval < 1) return fail(CHESS_ERR_CONFIG, "fixed interval must be >= 1 page");
+  if (cfg->mode != 0 && cfg->mode != 1) return fail(CHESS_ERR_VALUE, "unknown trigger mode %d", cfg->mode);
+  return launch_record_entropy(*st, entropy, active, *cfg, (cudaStream_t)stream);
+}
+
+int chess_select(const ChessState* st, const ChessSelectCfg* cfg, void* stream) {
+  Workspace ws;
+  int rc = state_ws(st, &ws);
+  if (rc) return rc;
+  if (!cfg) return fail(CHESS_ERR_CONFIG, "null select cfg");
+  const double r[3] = {cfg->rho_grid, cfg->rho_chunk, cfg->rho_page};
+  for (int i = 0; i < 3; ++i)
+    if (!(r[i] > 0.0 && r[i] <= 1.0)) return fail(CHESS_ERR_CONFIG, "ratios must be in (0, 1]");
+  SelParams prm;
+  prm.rho[0] = r[0];
+  prm.rho[1] = r[1];
+  prm.rho[2] = r[2];
+  prm.full_scan = cfg->full_scan;
+  prm.force_all = cfg->force_all;
+  const int grid = 4 * num_sms();
+  return launch_select(*st, ws, prm, grid, (cudaStream_t)stream);
+}
+
+int chess_build_working_set(const ChessState* st, void* stream) {
+  Workspace ws;
+  int rc = state_ws(st, &ws);
+  if (rc) return rc;
+  return launch_build_ws_all(*st, (cudaStream_t)stream);
+}
+
+int chess_sparse_decode(const ChessState* st, int32_t layer, const void* q, int64_t q_stride,
+                        void* out, int64_t out_stride, float* lse, float softmax_scale,
+                        void* stream) {
+  Workspace ws;
+  int rc = state_ws(st, &ws);
+  if (rc) return rc;
+  if (layer < 0 || layer >= st->d.layers) return fail(CHESS_ERR_INDEX, "layer %d out of range", layer);
+  if (!q || !out) return fail(CHESS_ERR_SHAPE, "sparse_decode: null q/out");
+  const int64_t row = (int64_t)st->d.q_heads * st->d.head_dim;
+  if (q_stride < row || out_stride < row) return fail(CHESS_ERR_SHAPE, "sparse_decode: stride < q_heads*head_dim");
+  return launch_sparse_decode(*st, ws, layer, q, q_stride, out, out_stride, lse, softmax_scale,
+                              (cudaStream_t)stream);
+}
+
+int chess_entropy_trigger(const ChessState* st, const float* logits, int64_t vocab, int64_t ld,
+                          const ChessTriggerCfg* cfg, double* entropy_out, void* stream) {
+  Workspace ws;
+  int rc = state_ws(st, &ws);
+  if (rc) return rc;
+  if (!cfg || !logits || vocab < 1 || ld < vocab) return fail(CHESS_ERR_SHAPE, "entropy_trigger: bad logits");
+  if (cfg->policy < 0 || cfg->policy > 4) return fail(CHESS_ERR_CONFIG, "unknown policy %d", cfg->policy);
+  if (cfg->policy == CHESS_POLICY_FIXED && cfg->interval < 1) return fail(CHESS_ERR_CONFIG, "fixed interval must be >= 1 page");
+  if (cfg->mode != 0 && cfg->mode != 1) return fail(CHESS_ERR_VALUE, "unknown trigger mode %d", cfg->mode);
+  return launch_entropy_trigger(*st, ws, logits, vocab, ld, *cfg, entropy_out, (cudaStream_t)stream);
+}
+
+int chess_score_rows(const void* rows, int32_t dtype, int64_t n_rows, int64_t dim, int64_t ld,
+                     const double* anchor, double* scores, void* stream) {
+  if (n_rows < 0 || dim < 0 || ld < dim) return fail(CHESS_ERR_SHAPE, "score_rows: bad shape");
+  if (dtype < 0 || dtype > 2) return fail(CHESS_ERR_CONFIG, "bad dtype");
+  return launch_score_rows(rows, dtype, n_rows, dim, ld, anchor, scores, (cudaStream_t)stream);
+}
+
+int chess_mean_rows(const void* rows, int32_t dtype, int64_t n_rows, int64_t dim, int64_t ld,
+                    double* out, void* stream) {
+  if (n_rows < 1) return fail(CHESS_ERR_EMPTY_CONTEXT, "no rows to average");
+  if (dim < 0 || ld < dim) return fail(CHESS_ERR_SHAPE, "mean_rows: bad shape");
+  if (dim == 0) return CHESS_OK;
+  return launch_mean_rows(rows, dtype, n_rows, dim, ld, out, (cudaStream_t)stream);
+}
+
+int chess_prune(const double* s_g, int32_t G, const double* s_c, int32_t C, const double* s_p,
+                int32_t P, const int64_t* page_to_chunk, const int64_t* chunk_to_grid,
+                double rho_grid, double rho_chunk, double rho_page, int32_t* out_pages,
+                int32_t* out_count, void* workspace, void* stream) {
+  if (G < 0 || C < 0 || P < 0) return fail(CHESS_ERR_SHAPE, "prune: negative sizes");
+  return launch_prune(s_g, G, s_c, C, s_p, P, page_to_chunk, chunk_to_grid, rho_grid, rho_chunk,
+                      rho_page, out_pages, out_count, workspace, (cudaStream_t)stream);
+}
+
+int chess_topk(const double* scores, int32_t n, int32_t k, const uint8_t* active,
+               int32_t* out_idx, int32_t* out_count, int32_t sorted, void* workspace,
+               void* stream) {
+  if (n < 0) return fail(CHESS_ERR_SHAPE, "topk: negative n");
+  return launch_topk(scores, n, k, active, out_idx, out_count, sorted, workspace,
+                     (cudaStream_t)stream);
+}
+
+int chess_working_set(const int32_t* selected, int32_t n_sel, int32_t n_pages, int32_t window,
+                      int32_t sinks, const int32_t* page_table, int32_t* out_pages,
+                      int8_t* out_prov, int32_t* out_phys, int32_t* out_len, void* stream) {
+  if (window < 1) return fail(CHESS_ERR_CONFIG, "window_pages must be >= 1");
+  if (sinks < 0) return fail(CHESS_ERR_CONFIG, "sink_pages must be >= 0");
+  if (n_pages < 0 || n_sel < 0) return fail(CHESS_ERR_SHAPE, "working_set: negative sizes");
+  return launch_working_set(selected, n_sel, n_pages, window, sinks, page_table, out_pages,
+                            out_prov, out_phys, out_len, (cudaStream_t)stream);
+}
+
+int chess_gather_pages(const int32_t* page_table, int32_t n_pages, const int64_t* idx, int32_t n,
+                       int32_t* out, int32_t* err, void* stream) {
+  return launch_gather_pages(page_table, n_pages, idx, n, out, err, (cudaStream_t)stream);
+}
+
+int chess_entropy_probs(const double* probs, int64_t rows, int64_t n, int64_t ld, double* out,
+                        int32_t* flags, void* stream) {
+  if (rows < 0 || n < 1 || ld < n) return fail(CHESS_ERR_SHAPE, "entropy_probs: bad shape");
+  return launch_entropy_probs(probs, rows, n, ld, out, flags, (cudaStream_t)stream);
+}
+
+size_t chess_entropy_workspace_bytes(int64_t rows) {
+  return (size_t)rows * (kEntSplit * 3 * 8 + 8) + 512;
+}
+
+int chess_entropy_logits(const float* logits, int64_t rows, int64_t vocab, int64_t ld, double* out,
+                         void* workspace, void* stream) {
+  if (rows < 0 || vocab < 1 || ld < vocab) return fail(CHESS_ERR_SHAPE, "entropy_logits: bad shape");
+  if (rows == 0) return CHESS_OK;
+  Workspace ws{};
+  uint8_t* p = reinterpret_cast<uint8_t*>(workspace);
+  ws.ent_done = reinterpret_cast<int32_t*>(p);
+  ws.ent_part = reinterpret_cast<double*>(p + ((rows * 4 + 255) / 256) * 256);
+  return launch_entropy_logits(ws, logits, rows, vocab, ld, out, (cudaStream_t)stream);
+}
+
+int chess_page_uncertainty(const double* ent, int32_t n, double* out, void* stream) {
+  if (n < 1) return fail(CHESS_ERR_VALUE, "page has no generated tokens");
+
+  return launch_page_uncertainty(ent, n, out, (cudaStream_t)stream);
+}
+
+}  // extern "C"

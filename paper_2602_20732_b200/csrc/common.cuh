@@ -1,0 +1,409 @@
+// common.cuh — shared device helpers for the CHESS B200 kernels (sm_100a).
+//
+// Contents: error plumbing for the C-ABI, bf16 helpers, mbarrier +
+// cp.async.bulk (TMA 1-D bulk copy) PTX wrappers, f64 helpers that reproduce
+// NumPy's summation orders bit-for-bit, the orderable score key used by every
+// top-k (ties to the lower index, selection.py:77-88), and a block-wide radix
+// select.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cstdio>
+#include <cstring>
+
+#include "../../include/chess_b200.h"
+
+namespace chess {
+
+// ---------------------------------------------------------------------------
+// host-side error plumbing
+// ---------------------------------------------------------------------------
+void set_error(const char* fmt, ...);
+int fail(int code, const char* fmt, ...);
+int check_launch(const char* what);
+int num_sms();
+
+__host__ __device__ inline int64_t max_chunks(const ChessDims& d) {
+  return (d.max_pages + d.pages_per_chunk - 1) / d.pages_per_chunk;
+}
+__host__ __device__ inline int64_t max_grids(const ChessDims& d) {
+  return (max_chunks(d) + d.chunks_per_grid - 1) / d.chunks_per_grid;
+}
+__host__ __device__ inline int64_t max_rows(const ChessDims& d) { return d.max_pages + max_chunks(d) + max_grids(d); }
+
+// ---------------------------------------------------------------------------
+// workspace layout (carved from ChessState::workspace, see capi.cu)
+// ---------------------------------------------------------------------------
+constexpr int kScanSlice = 2048;   // elements of one (row, slice) work unit
+constexpr int kScanRows = 8;       // rows per work item
+constexpr int kScanThreads = 256;
+constexpr int kMaxBatch = 1024;
+
+struct Workspace {
+  int32_t* sel_done;     // [batch]
+  int32_t* cand;         // [batch][3][max_rows]  candidate row ids per level
+  int32_t* cand_n;       // [batch][4]            candidate counts (levels 0..2, full)
+  double* scores;        // [batch][max_rows]     reduced scores of the current level
+  uint64_t* keys;        // [batch][max_rows]
+  double* part;          // [batch][max_rows][n_slices]
+  int32_t* kept;         // [batch][max_rows]
+  int32_t* plist;        // [batch][max_rows]  kept parents (ascending)
+  int32_t* attn_done;    // [batch*kv_heads]
+  float* attn_part;      // [(batch*kv_heads + attn_ctas)][q_per_kv][head_dim + 2]
+  int32_t* ent_done;     // [batch]
+  double* ent_part;      // [batch][kEntSplit][3]
+  int32_t* append_done;  // [batch]
+  int32_t* seal_done;    // [batch]
+  int32_t attn_ctas;
+  int32_t n_slices;
+};
+
+constexpr int kEntSplit = 16;
+constexpr int kAttnCtasMax = 148 * 4;
+
+size_t workspace_layout(const ChessDims& d, void* base, Workspace* ws);
+
+struct SelParams {
+  double rho[3];
+  int32_t full_scan;
+  int32_t force_all;
+};
+
+// ---------------------------------------------------------------------------
+// device helpers
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ float bf2f(__nv_bfloat16 x) { return __bfloat162float(x); }
+
+__device__ __forceinline__ float2 bf2x2f(uint32_t packed) {
+  float2 r;
+  r.x = __uint_as_float(packed << 16);
+  r.y = __uint_as_float(packed & 0xffff0000u);
+  return r;
+}
+
+// Orderable key for f64 scores: larger score -> larger key.  -0.0 is
+// canonicalised to +0.0 (NumPy compares them equal, stable order decides) and
+// NaN sorts below -inf (argsort of -scores puts NaN last).
+__device__ __forceinline__ uint64_t score_key(double s) {
+  if (s != s) return 0ull;
+  if (s == 0.0) s = 0.0;
+  uint64_t b = (uint64_t)__double_as_longlong(s);
+  return (b & 0x8000000000000000ull) ? ~b : (b | 0x8000000000000000ull);
+}
+
+// NumPy pairwise summation of a contiguous f64 vector (numpy
+// DOUBLE_pairwise_sum, blocks of 8 accumulators up to 128 elements).  Used for
+// page statistics (uncertainty.py:41-48 -> np.mean) so device results are
+// bit-identical to the reference given identical inputs.
+template <typename F>
+__device__ __forceinline__ double np_pairwise_leaf(F at, int off, int n) {
+  if (n < 8) {
+    double r = 0.0;
+    for (int i = 0; i < n; ++i) r = __dadd_rn(r, at(off + i));
+    return r;
+  }
+  double r[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) r[j] = at(off + j);
+  int i = 8;
+  for (; i < n - (n % 8); i += 8) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], at(off + i + j));
+  }
+  double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                         __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+  for (; i < n; ++i) res = __dadd_rn(res, at(off + i));
+  return res;
+}
+
+// Non-recursive evaluation of NumPy's pairwise tree (n > 128 splits at
+// n2 = n/2 rounded down to a multiple of 8) with an explicit stack.
+template <typename F>
+__device__ double np_pairwise(F at, int n) {
+  if (n <= 128) return np_pairwise_leaf(at, 0, n);
+  int st_off[40], st_n[40], st_phase[40];
+  double st_left[40];
+  int sp = 0;
+  st_off[0] = 0; st_n[0] = n; st_phase[0] = 0;
+  double ret = 0.0;
+  while (sp >= 0) {
+    const int off = st_off[sp], m = st_n[sp];
+    if (m <= 128) {
+      ret = np_pairwise_leaf(at, off, m);
+      --sp;
+      continue;
+    }
+    int m2 = m / 2;
+    m2 -= m2 % 8;
+    if (st_phase[sp] == 0) {  // descend left
+      st_phase[sp] = 1;
+      ++sp;
+      st_off[sp] = off; st_n[sp] = m2; st_phase[sp] = 0;
+    } else if (st_phase[sp] == 1) {  // left done -> descend right
+      st_left[sp] = ret;
+      st_phase[sp] = 2;
+      ++sp;
+      st_off[sp] = off + m2; st_n[sp] = m - m2; st_phase[sp] = 0;
+    } else {  // both done
+      ret = __dadd_rn(st_left[sp], ret);
+      --sp;
+    }
+  }
+  return ret;
+}
+
+__device__ __forceinline__ double np_pairwise_sum(const double* a, int n, int stride) {
+  return np_pairwise([=](int i) { return a[(int64_t)i * stride]; }, n);
+}
+
+// ---------------------------------------------------------------------------
+// mbarrier + TMA bulk copy (cp.async.bulk) wrappers
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void fence_barrier_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  while (!mbar_try_wait(bar, parity)) {
+  }
+}
+// 1-D bulk global->shared copy completing on an mbarrier (SASS: UBLKCP).
+__device__ __forceinline__ void tma_load_1d(void* dst_smem, const void* src_gmem, uint32_t bytes,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst_smem)),
+      "l"(src_gmem), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// Programmatic dependent launch controls (griddepcontrol, sm_90+).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+__device__ __forceinline__ double shfl_xor_d(double v, int m) {
+  return __shfl_xor_sync(0xffffffffu, v, m);
+}
+
+// ---------------------------------------------------------------------------
+// block-wide helpers (blockDim.x == NT, multiple of 32)
+// ---------------------------------------------------------------------------
+template <int NT>
+__device__ __forceinline__ int block_exclusive_scan(int v, int* smem_warp, int* total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) smem_warp[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    int w = (lane < NT / 32) ? smem_warp[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int y = __shfl_up_sync(0xffffffffu, w, o);
+      if (lane >= o) w += y;
+    }
+    if (lane < NT / 32) smem_warp[lane] = w;
+  }
+  __syncthreads();
+  int base = warp > 0 ? smem_warp[warp - 1] : 0;
+  *total = smem_warp[NT / 32 - 1];
+  __syncthreads();
+  return base + x - v;
+}
+
+// Block-wide top-k selection over n keys (keys[i] = score_key(score), entries
+// in increasing index order).  Marks keep[i] = 1 for exactly min(k, n)
+// entries: all keys above the k-th largest key, plus the lowest-index entries
+// equal to it (ties to the lower index, selection.py:77-88).  Radix select
+// over 8 digits of 8 bits.  smem: 256 ints hist + 40 ints scratch.
+template <int NT>
+__device__ void block_topk_mark(const uint64_t* keys, int n, int k, int* keep, int* s_hist,
+                                int* s_scratch) {
+  if (k >= n) {
+    for (int i = threadIdx.x; i < n; i += NT) keep[i] = 1;
+    __syncthreads();
+    return;
+  }
+  if (k <= 0) {
+    for (int i = threadIdx.x; i < n; i += NT) keep[i] = 0;
+    __syncthreads();
+    return;
+  }
+  uint64_t prefix = 0, mask = 0;
+  int kk = k;  // how many still to take among keys matching prefix
+  for (int shift = 56; shift >= 0; shift -= 8) {
+    for (int b = threadIdx.x; b < 256; b += NT) s_hist[b] = 0;
+    __syncthreads();
+    for (int i = threadIdx.x; i < n; i += NT) {
+      uint64_t key = keys[i];
+      if ((key & mask) == prefix) atomicAdd(&s_hist[(key >> shift) & 255], 1);
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      // lane l owns bins [255-8l-7, 255-8l] (descending digit order)
+      const int lane = threadIdx.x;
+      int c[8];
+      int tot = 0;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        c[j] = s_hist[255 - (lane * 8 + j)];
+        tot += c[j];
+      }
+      int incl = tot;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      int excl = incl - tot;  // count of keys in higher digits (owned by lower lanes)
+      // find digit where cumulative count reaches kk
+      int found_digit = -1, above = 0;
+      if (excl < kk && incl >= kk) {
+        int run = excl;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          if (found_digit < 0) {
+            if (run + c[j] >= kk) {
+              found_digit = 255 - (lane * 8 + j);
+              above = run;
+            } else {
+              run += c[j];
+            }
+          }
+        }
+        s_scratch[0] = found_digit;
+        s_scratch[1] = above;
+      }
+    }
+    __syncthreads();
+    const int digit = s_scratch[0];
+    kk -= s_scratch[1];
+    prefix |= ((uint64_t)digit) << shift;
+    mask |= 0xFFull << shift;
+    __syncthreads();
+  }
+  // prefix == k-th largest key T; take all keys > T and the first kk keys == T.
+  const uint64_t T = prefix;
+  int taken_eq = 0;
+  for (int base = 0; base < n; base += NT) {
+    int i = base + threadIdx.x;
+    uint64_t key = i < n ? keys[i] : 0ull;
+    int eq = (i < n && key == T) ? 1 : 0;
+    int tot;
+    int pos = block_exclusive_scan<NT>(eq, s_scratch + 8, &tot);
+    if (i < n) keep[i] = (key > T) || (eq && (taken_eq + pos) < kk);
+    taken_eq += tot;
+  }
+  __syncthreads();
+}
+
+// Working set of slot s from its sorted semantic list + window + sinks, then
+// gathered through the page table into the block table (selection.py:126-140,
+// kv_store.py:156-166).  Sorted output falls out of the region structure:
+// [0, ns) sinks | semantic in [ns, w0) | [max(w0, ns), n) window.
+template <int NT>
+__device__ void block_build_ws(const ChessState& st, int s, int* s_scratch) {
+  const ChessDims& d = st.d;
+  const int n = st.num_pages[s];
+  const int ns = min(st.sink_count[s], n);
+  const int w0 = max(0, n - d.window_pages);
+  const int c0 = max(w0, ns);
+  const int32_t* sem = st.semantic + (int64_t)s * d.max_pages;
+  if (threadIdx.x == 0) {
+    const int nsem = st.n_semantic[s];
+    int lo = 0, hi = nsem;
+    while (lo < hi) {  // first entry >= ns
+      int mid = (lo + hi) >> 1;
+      if (sem[mid] < ns) lo = mid + 1; else hi = mid;
+    }
+    int a = lo;
+    hi = nsem;
+    while (lo < hi) {  // first entry >= w0
+      int mid = (lo + hi) >> 1;
+      if (sem[mid] < w0) lo = mid + 1; else hi = mid;
+    }
+    s_scratch[0] = a;
+    s_scratch[1] = max(a, lo);
+  }
+  __syncthreads();
+  const int lo = s_scratch[0], hi = s_scratch[1];
+  int total = ns + (hi - lo) + (n - c0);
+  const int cap = d.max_ws;
+  int32_t* wl = st.ws_logical + (int64_t)s * cap;
+  int32_t* bt = st.block_table + (int64_t)s * cap;
+  int8_t* pv = st.ws_prov + (int64_t)s * cap;
+  const int32_t* pt = st.page_table + (int64_t)s * d.max_pages;
+  for (int i = threadIdx.x; i < total && i < cap; i += NT) {
+    int lp;
+    int8_t tag;
+    if (i < ns) {
+      lp = i;
+      tag = CHESS_PROV_SINK;
+    } else if (i < ns + (hi - lo)) {
+      lp = sem[lo + i - ns];
+      tag = CHESS_PROV_SEMANTIC;
+    } else {
+      lp = c0 + (i - ns - (hi - lo));
+      tag = CHESS_PROV_WINDOW;
+    }
+    wl[i] = lp;
+    bt[i] = pt[lp];
+    pv[i] = tag;
+  }
+  if (threadIdx.x == 0) st.ws_len[s] = min(total, cap);
+  __syncthreads();
+}
+
+// Ordered compaction: out[pos] = idx_of(i) for keep[i] != 0, i ascending.
+template <int NT, typename F>
+__device__ int block_compact(const int* keep, int n, int* out, int* s_scratch, F idx_of) {
+  int count = 0;
+  for (int base = 0; base < n; base += NT) {
+    int i = base + threadIdx.x;
+    int f = (i < n && keep[i]) ? 1 : 0;
+    int tot;
+    int pos = block_exclusive_scan<NT>(f, s_scratch, &tot);
+    if (f) out[count + pos] = idx_of(i);
+    count += tot;
+  }
+  return count;
+}
+
+}  // namespace chess

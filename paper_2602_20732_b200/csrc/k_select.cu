@@ -1,0 +1,680 @@
+// k_select.cu — K2 anchor scoring + K3 coarse-to-fine masked top-k cascade.
+//
+// Reference: selection.py:44-140
+//   score_all           :62-74   scores = V_all @ anchor (one GEMV)
+//   _top_k              :77-88   top ceil(rho*active), ties -> lower index
+//   hierarchical_prune  :91-111  grids -> chunks of kept grids -> pages
+//   reconstruct_working_set :126-140, gather_pages kv_store.py:156-166
+//
+// Design: the scan is a batched GEMV that is HBM-bound at
+// 0.25-0.5 flop/B, far below the tcgen05 ridge, so it runs on the FP64 pipe:
+// f32 (or f64) summary rows x f64 anchor, accumulated in f64.  The
+// conditional scan only scores children of kept parents, which is
+// output-identical to Alg.1's full scan (a masked top-k can never keep a
+// child of a pruned parent); `full_scan` keeps the literal one-GEMV variant.
+//
+// Work decomposition: an item is (slot, 8 candidate rows, 2048-element slice).
+// Persistent CTAs stride over items; per-(row, slice) partials land in the
+// workspace and the last CTA to finish a slot's items (atomic counter) reduces
+// them in fixed slice order (deterministic), runs the radix top-k and writes
+// the next level's candidate list, or — at the page level — the semantic set,
+// working set and block table.
+#include "common.cuh"
+
+namespace chess {
+
+namespace {
+
+constexpr int kNT = kScanThreads;
+constexpr int kWarps = kNT / 32;
+
+__device__ __forceinline__ int slot_pages(const ChessState& st, int s) { return st.num_sealed[s]; }
+
+struct LevelShape {
+  int P, C, G;
+};
+__device__ __forceinline__ LevelShape shape_of(const ChessState& st, int s) {
+  LevelShape sh;
+  sh.P = st.num_sealed[s];
+  sh.C = (sh.P + st.d.pages_per_chunk - 1) / st.d.pages_per_chunk;
+  sh.G = (sh.C + st.d.chunks_per_grid - 1) / st.d.chunks_per_grid;
+  return sh;
+}
+
+__device__ __forceinline__ bool fired(const ChessState& st, const SelParams& prm, int s) {
+  return prm.force_all || (st.fire != nullptr && st.fire[s] != 0);
+}
+
+// number of candidate rows of slot s at this level
+__device__ __forceinline__ int level_rows(const ChessState& st, const Workspace& ws,
+                                          const SelParams& prm, int s, int level) {
+  if (!fired(st, prm, s)) return 0;
+  const LevelShape sh = shape_of(st, s);
+  if (sh.P == 0) return 0;
+  if (level == 0) return sh.G;
+  if (level == 3) return sh.G + sh.C + sh.P;
+  return ws.cand_n[4 * s + level];
+}
+
+template <typename T>
+__device__ __forceinline__ const T* level_row_ptr(const ChessState& st, const Workspace& ws, int s,
+                                                  int level, int i, const LevelShape& sh);
+
+template <>
+__device__ __forceinline__ const float* level_row_ptr<float>(const ChessState& st,
+                                                             const Workspace& ws, int s, int level,
+                                                             int i, const LevelShape& sh) {
+  const ChessDims& d = st.d;
+  const int64_t mr = max_rows(d);
+  int which, row;
+  if (level == 3) {
+    which = i < sh.G ? 0 : (i < sh.G + sh.C ? 1 : 2);
+    row = which == 0 ? i : (which == 1 ? i - sh.G : i - sh.G - sh.C);
+  } else {
+    which = level;
+    row = level == 0 ? i : ws.cand[((int64_t)s * 3 + level) * mr + i];
+  }
+  if (which == 0) return st.grid_vec32 + ((int64_t)s * max_grids(d) + row) * d.ld;
+  if (which == 1) return st.chunk_vec32 + ((int64_t)s * max_chunks(d) + row) * d.ld;
+  return st.page_vec32 + ((int64_t)s * d.max_pages + row) * d.ld;
+}
+
+template <>
+__device__ __forceinline__ const double* level_row_ptr<double>(const ChessState& st,
+                                                               const Workspace& ws, int s,
+                                                               int level, int i,
+                                                               const LevelShape& sh) {
+  const ChessDims& d = st.d;
+  const int64_t mr = max_rows(d);
+  int which, row;
+  if (level == 3) {
+    which = i < sh.G ? 0 : (i < sh.G + sh.C ? 1 : 2);
+    row = which == 0 ? i : (which == 1 ? i - sh.G : i - sh.G - sh.C);
+  } else {
+    which = level;
+    row = level == 0 ? i : ws.cand[((int64_t)s * 3 + level) * mr + i];
+  }
+  if (which == 0) return st.grid_vec64 + ((int64_t)s * max_grids(d) + row) * d.ld;
+  if (which == 1) return st.chunk_vec64 + ((int64_t)s * max_chunks(d) + row) * d.ld;
+  return st.page_vec64 + ((int64_t)s * d.max_pages + row) * d.ld;
+}
+
+// 8 elements per thread of a 2048-element slice: element offsets within the
+// slice for vector group v (f32: 2 x float4, f64: 4 x double2).
+template <typename T>
+struct SliceMap;
+template <>
+struct SliceMap<float> {
+  static constexpr int kGroups = 2;
+  static constexpr int kVec = 4;
+  __device__ static int off(int v) { return v * 1024 + (int)threadIdx.x * 4; }
+};
+template <>
+struct SliceMap<double> {
+  static constexpr int kGroups = 4;
+  static constexpr int kVec = 2;
+  __device__ static int off(int v) { return v * 512 + (int)threadIdx.x * 2; }
+};
+
+template <typename T>
+__device__ __forceinline__ void load_group(const T* p, T* out);
+template <>
+__device__ __forceinline__ void load_group<float>(const float* p, float* out) {
+  const float4 v = __ldcs(reinterpret_cast<const float4*>(p));
+  out[0] = v.x;
+  out[1] = v.y;
+  out[2] = v.z;
+  out[3] = v.w;
+}
+template <>
+__device__ __forceinline__ void load_group<double>(const double* p, double* out) {
+  const double2 v = __ldcs(reinterpret_cast<const double2*>(p));
+  out[0] = v.x;
+  out[1] = v.y;
+}
+
+// ---------------------------------------------------------------------------
+// tail: reduce partials, top-k, emit next level (block-wide, one slot)
+// ---------------------------------------------------------------------------
+struct TailSmem {
+  int hist[256];
+  int scratch[64];
+};
+
+__device__ void expand_children(const int* parents, int m, int fan, int total_children, int* out,
+                                int* out_n) {
+  // all parents except possibly the globally last have exactly `fan` children
+  int count = 0;
+  if (m > 0) {
+    const int last = parents[m - 1];
+    count = (m - 1) * fan + min(fan, total_children - last * fan);
+  }
+  for (int idx = threadIdx.x; idx < count; idx += kNT) {
+    const int r = idx / fan, c = idx - r * fan;
+    out[idx] = parents[r] * fan + c;
+  }
+  if (threadIdx.x == 0) *out_n = count;
+}
+
+__device__ void select_tail(const ChessState& st, const Workspace& ws, const SelParams& prm, int s,
+                            int level, int n, TailSmem& sm) {
+  const ChessDims& d = st.d;
+  const int64_t mr = max_rows(d);
+  const int ns = ws.n_slices;
+  double* sc = ws.scores + (int64_t)s * mr;
+  uint64_t* keys = ws.keys + (int64_t)s * mr;
+  int* kept = ws.kept + (int64_t)s * mr;
+  int* plist = ws.plist + (int64_t)s * mr;
+  const double* part = ws.part + (int64_t)s * mr * ns;
+  const LevelShape sh = shape_of(st, s);
+  int* stats = st.sel_stats + 8 * s;
+
+  // fixed-order reduction over slices (deterministic)
+  for (int i = threadIdx.x; i < n; i += kNT) {
+    double acc = __ldcg(part + (int64_t)i * ns);
+    for (int q = 1; q < ns; ++q) acc = __dadd_rn(acc, __ldcg(part + (int64_t)i * ns + q));
+    sc[i] = acc;
+  }
+  __syncthreads();
+
+  // level order to run in this tail
+  const int lv_begin = level == 3 ? 0 : level;
+  const int lv_end = level == 3 ? 3 : level + 1;
+  int* cand1 = ws.cand + ((int64_t)s * 3 + 1) * mr;
+  int* cand2 = ws.cand + ((int64_t)s * 3 + 2) * mr;
+  for (int lv = lv_begin; lv < lv_end; ++lv) {
+    // candidate count and ids at this level
+    int m;
+    const int* cand = nullptr;
+    if (lv == 0) {
+      m = sh.G;
+    } else {
+      m = ws.cand_n[4 * s + lv];
+      cand = lv == 1 ? cand1 : cand2;
+    }
+    // keys of the candidates
+    for (int i = threadIdx.x; i < m; i += kNT) {
+      double v;
+      if (level == 3) {
+        const int id = cand ? cand[i] : i;
+        const int off = lv == 0 ? 0 : (lv == 1 ? sh.G : sh.G + sh.C);
+        v = sc[off + id];
+      } else {
+        v = sc[i];
+      }
+      keys[i] = score_key(v);
+    }
+    __syncthreads();
+    // ceil in double (selection.py:98, 103, 108)
+    const int k = (int)ceil(prm.rho[lv] * (double)m);
+    block_topk_mark<kNT>(keys, m, k, kept, sm.hist, sm.scratch);
+    const int fan = lv == 0 ? d.chunks_per_grid : d.pages_per_chunk;
+    int kcount;
+    if (lv < 2) {
+      kcount = block_compact<kNT>(kept, m, plist, sm.scratch,
+                                  [&](int i) { return cand ? cand[i] : i; });
+      __syncthreads();
+      const int total_children = lv == 0 ? sh.C : sh.P;
+      int* out = lv == 0 ? cand1 : cand2;
+      expand_children(plist, kcount, fan, total_children, out, &ws.cand_n[4 * s + lv + 1]);
+      if (threadIdx.x == 0) {
+        stats[5 + lv] = kcount;
+        stats[3 + lv] = (kcount > 0) ? (kcount - 1) * fan + min(fan, total_children - plist[kcount - 1] * fan) : 0;
+      }
+    } else {
+      int32_t* sem = st.semantic + (int64_t)s * d.max_pages;
+      kcount = block_compact<kNT>(kept, m, sem, sm.scratch, [&](int i) { return cand[i]; });
+      if (threadIdx.x == 0) {
+        st.n_semantic[s] = kcount;
+        stats[7] = kcount;
+        stats[0] = sh.G;
+        stats[1] = sh.C;
+        stats[2] = sh.P;
+      }
+    }
+    __syncthreads();
+    __threadfence_block();
+  }
+  if (lv_end == 3) block_build_ws<kNT>(st, s, sm.scratch);
+}
+
+// slots that fired with an empty index: empty semantic set + WS refresh
+__device__ void handle_empty_slots(const ChessState& st, const Workspace& ws, const SelParams& prm,
+                                   TailSmem& sm) {
+  for (int s = 0; s < st.d.batch; ++s) {
+    if (!fired(st, prm, s) || st.num_sealed[s] != 0) continue;
+    if (threadIdx.x == 0) {
+      st.n_semantic[s] = 0;
+      ws.cand_n[4 * s + 1] = 0;
+      ws.cand_n[4 * s + 2] = 0;
+      for (int i = 0; i < 8; ++i) st.sel_stats[8 * s + i] = 0;
+    }
+    __syncthreads();
+    block_build_ws<kNT>(st, s, sm.scratch);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// the scan kernel (one launch per level; level 3 = Alg.1 full scan)
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void __launch_bounds__(kNT, 1) select_scan_kernel(ChessState st, Workspace ws,
+                                                          SelParams prm, int level) {
+  extern __shared__ int s_prefix[];  // [batch + 1]
+  __shared__ double s_wpart[kScanRows][kWarps];
+  __shared__ TailSmem sm;
+  __shared__ int s_last;
+  const ChessDims& d = st.d;
+  const int nb = d.batch;
+  const int nsl = ws.n_slices;
+
+  if ((level == 0 || level == 3) && blockIdx.x == 0) handle_empty_slots(st, ws, prm, sm);
+
+  // per-slot item counts -> prefix (block scan in tiles of kNT)
+  int running = 0;
+  for (int b0 = 0; b0 < nb; b0 += kNT) {
+    const int s = b0 + threadIdx.x;
+    int items = 0;
+    if (s < nb) {
+      const int n = level_rows(st, ws, prm, s, level);
+      items = ((n + kScanRows - 1) / kScanRows) * nsl;
+    }
+    int tot;
+    const int pos = block_exclusive_scan<kNT>(items, sm.scratch, &tot);
+    if (s < nb) s_prefix[s] = running + pos;
+    running += tot;
+  }
+  if (threadIdx.x == 0) s_prefix[nb] = running;
+  __syncthreads();
+  const int total = running;
+
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int it = blockIdx.x; it < total; it += gridDim.x) {
+    // slot of this item: last s with s_prefix[s] <= it
+    int lo = 0, hi = nb;
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (s_prefix[mid] <= it) lo = mid; else hi = mid;
+    }
+    const int s = lo;
+    const int local = it - s_prefix[s];
+    const int rb = local / nsl, slice = local - rb * nsl;
+    const int n = level_rows(st, ws, prm, s, level);
+    const int r0 = rb * kScanRows;
+    const int64_t ebase = (int64_t)slice * kScanSlice;
+    const LevelShape sh = shape_of(st, s);
+
+    // anchor slice (f64) in registers
+    const double* anc = st.anchor + (int64_t)s * d.ld + ebase;
+    double a[8];
+#pragma unroll
+    for (int v = 0; v < SliceMap<T>::kGroups; ++v) {
+      const int o = SliceMap<T>::off(v);
+#pragma unroll
+      for (int e = 0; e < SliceMap<T>::kVec; e += 2) {
+        double2 x = make_double2(0.0, 0.0);
+        if (ebase + o < d.ld) x = *reinterpret_cast<const double2*>(anc + o + e);
+        a[v * SliceMap<T>::kVec + e] = x.x;
+        a[v * SliceMap<T>::kVec + e + 1] = x.y;
+      }
+    }
+    // row loads (a phase's rows issued before use for MLP), f64 accumulation.
+    // f32 rows: 8 rows in flight (64 KB per CTA); f64 rows: 2 phases of 4.
+    constexpr int kPhases = sizeof(T) == 8 ? 2 : 1;
+    constexpr int kRowsPh = kScanRows / kPhases;
+    double acc[kScanRows];
+#pragma unroll
+    for (int phs = 0; phs < kPhases; ++phs) {
+      T vals[kRowsPh][8];
+#pragma unroll
+      for (int rr = 0; rr < kRowsPh; ++rr) {
+        const int r = phs * kRowsPh + rr;
+        const bool row_ok = (r0 + r) < n;
+        const T* rp = row_ok ? level_row_ptr<T>(st, ws, s, level, r0 + r, sh) + ebase : nullptr;
+#pragma unroll
+        for (int v = 0; v < SliceMap<T>::kGroups; ++v) {
+          const int o = SliceMap<T>::off(v);
+          if (row_ok && ebase + o < d.ld) {
+            load_group<T>(rp + o, &vals[rr][v * SliceMap<T>::kVec]);
+          } else {
+#pragma unroll
+            for (int e = 0; e < SliceMap<T>::kVec; ++e) vals[rr][v * SliceMap<T>::kVec + e] = T(0);
+          }
+        }
+      }
+#pragma unroll
+      for (int rr = 0; rr < kRowsPh; ++rr) {
+        double x = 0.0;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) x = __fma_rn(a[e], (double)vals[rr][e], x);
+        acc[phs * kRowsPh + rr] = x;
+      }
+    }
+    // warp transpose-reduce of 8 row partials: 4+2+1 exchanges, then 2 xor adds.
+    {
+      const bool b4 = lane & 16;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const double send = b4 ? acc[i] : acc[4 + i];
+        const double keep = b4 ? acc[4 + i] : acc[i];
+        acc[i] = keep + shfl_xor_d(send, 16);
+      }
+      const bool b3 = lane & 8;
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const double send = b3 ? acc[i] : acc[2 + i];
+        const double keep = b3 ? acc[2 + i] : acc[i];
+        acc[i] = keep + shfl_xor_d(send, 8);
+      }
+      const bool b2 = lane & 4;
+      {
+        const double send = b2 ? acc[0] : acc[1];
+        const double keep = b2 ? acc[1] : acc[0];
+        acc[0] = keep + shfl_xor_d(send, 4);
+      }
+      acc[0] += shfl_xor_d(acc[0], 2);
+      acc[0] += shfl_xor_d(acc[0], 1);
+      const int row = ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
+      if ((lane & 3) == 0) s_wpart[row][warp] = acc[0];
+    }
+    __syncthreads();
+    if (threadIdx.x < kScanRows && r0 + (int)threadIdx.x < n) {
+      double x = s_wpart[threadIdx.x][0];
+#pragma unroll
+      for (int w = 1; w < kWarps; ++w) x = __dadd_rn(x, s_wpart[threadIdx.x][w]);
+      ws.part[((int64_t)s * max_rows(d) + r0 + threadIdx.x) * nsl + slice] = x;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      const int items_s = s_prefix[s + 1] - s_prefix[s];
+      const int prev = atomicAdd(&ws.sel_done[s], 1);
+      s_last = (prev == items_s - 1);
+    }
+    __syncthreads();
+    if (s_last) {
+      __threadfence();
+      select_tail(st, ws, prm, s, level, n, sm);
+      if (threadIdx.x == 0) ws.sel_done[s] = 0;
+      __syncthreads();
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// generic function-level kernels
+// ---------------------------------------------------------------------------
+template <typename T>
+__device__ __forceinline__ double as_d(const T* p, int64_t i) { return (double)p[i]; }
+template <>
+__device__ __forceinline__ double as_d<__nv_bfloat16>(const __nv_bfloat16* p, int64_t i) {
+  return (double)bf2f(p[i]);
+}
+
+// score_all: one CTA per row, fixed-order f64 block reduction.
+template <typename T>
+__global__ void __launch_bounds__(256) score_rows_kernel(const T* rows, int64_t dim, int64_t ld,
+                                                         const double* anchor, double* scores) {
+  __shared__ double s_w[8];
+  const int64_t r = blockIdx.x;
+  const T* row = rows + r * ld;
+  double acc = 0.0;
+  for (int64_t j = threadIdx.x; j < dim; j += 256) acc = __fma_rn(anchor[j], as_d(row, j), acc);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += shfl_xor_d(acc, o);
+  if ((threadIdx.x & 31) == 0) s_w[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double x = s_w[0];
+    for (int w = 1; w < 8; ++w) x = __dadd_rn(x, s_w[w]);
+    scores[r] = x;
+  }
+}
+
+// hierarchical_prune with arbitrary maps (selection.py:91-111); one CTA.
+__global__ void __launch_bounds__(kNT) prune_kernel(const double* s_g, int G, const double* s_c,
+                                                    int C, const double* s_p, int P,
+                                                    const int64_t* p2c, const int64_t* c2g,
+                                                    double rg, double rc, double rp,
+                                                    int32_t* out_pages, int32_t* out_count,
+                                                    uint8_t* wsb) {
+  __shared__ TailSmem sm;
+  const int N = G + C + P;
+  uint64_t* keys = reinterpret_cast<uint64_t*>(wsb);
+  int* kept = reinterpret_cast<int*>(wsb + 8 * (size_t)N);
+  int* cand = kept + N;
+  int* mask = cand + N;  // [G + C] masks of kept grids, kept chunks
+  if (P == 0) {
+    if (threadIdx.x == 0) out_count[0] = out_count[1] = out_count[2] = 0;
+    return;
+  }
+  for (int lv = 0; lv < 3; ++lv) {
+    const int n_lv = lv == 0 ? G : (lv == 1 ? C : P);
+    const double* sc = lv == 0 ? s_g : (lv == 1 ? s_c : s_p);
+    // active candidates ascending
+    auto active = [&](int i) -> int {
+      if (lv == 0) return 1;
+      if (lv == 1) return mask[c2g[i]];
+      return mask[G + p2c[i]];
+    };
+    int m = 0;
+    for (int base = 0; base < n_lv; base += kNT) {
+      const int i = base + threadIdx.x;
+      const int f = (i < n_lv) ? active(i) : 0;
+      int tot;
+      const int pos = block_exclusive_scan<kNT>(f, sm.scratch, &tot);
+      if (f) cand[m + pos] = i;
+      m += tot;
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < m; i += kNT) keys[i] = score_key(sc[cand[i]]);
+    __syncthreads();
+    const double rho = lv == 0 ? rg : (lv == 1 ? rc : rp);
+    const int k = (int)ceil(rho * (double)m);
+    block_topk_mark<kNT>(keys, m, k, kept, sm.hist, sm.scratch);
+    if (lv < 2) {
+      int* mk = mask + (lv == 0 ? 0 : G);
+      for (int i = threadIdx.x; i < n_lv; i += kNT) mk[i] = 0;
+      __syncthreads();
+      for (int i = threadIdx.x; i < m; i += kNT)
+        if (kept[i]) mk[cand[i]] = 1;
+    } else {
+      const int cnt = block_compact<kNT>(kept, m, out_pages, sm.scratch, [&](int i) { return cand[i]; });
+      if (threadIdx.x == 0) out_count[0] = cnt;
+    }
+    __syncthreads();
+  }
+  // kept grid / chunk counts
+  int ng = 0, nc = 0;
+  for (int i = threadIdx.x; i < G; i += kNT) ng += mask[i];
+  for (int i = threadIdx.x; i < C; i += kNT) nc += mask[G + i];
+  int tot;
+  block_exclusive_scan<kNT>(ng, sm.scratch, &tot);
+  if (threadIdx.x == 0) out_count[1] = tot;
+  block_exclusive_scan<kNT>(nc, sm.scratch, &tot);
+  if (threadIdx.x == 0) out_count[2] = tot;
+}
+
+// masked top-k (selection.py:77-88 / oracle_flat_topk :114-123); one CTA.
+__global__ void __launch_bounds__(kNT) topk_kernel(const double* scores, int n, int k,
+                                                   const uint8_t* active, int32_t* out_idx,
+                                                   int32_t* out_count, int sorted, uint8_t* wsb) {
+  __shared__ TailSmem sm;
+  uint64_t* keys = reinterpret_cast<uint64_t*>(wsb);
+  int* kept = reinterpret_cast<int*>(wsb + 8 * (size_t)n);
+  int* cand = kept + n;
+  int m = 0;
+  for (int base = 0; base < n; base += kNT) {
+    const int i = base + threadIdx.x;
+    const int f = (i < n) ? (active ? (active[i] != 0) : 1) : 0;
+    int tot;
+    const int pos = block_exclusive_scan<kNT>(f, sm.scratch, &tot);
+    if (f) cand[m + pos] = i;
+    m += tot;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < m; i += kNT) keys[i] = score_key(scores[cand[i]]);
+  __syncthreads();
+  block_topk_mark<kNT>(keys, m, k, kept, sm.hist, sm.scratch);
+  const int cnt = min(max(k, 0), m);
+  if (sorted) {
+    block_compact<kNT>(kept, m, out_idx, sm.scratch, [&](int i) { return cand[i]; });
+  } else {
+    // descending score order, ties by index: rank among kept entries
+    for (int i = threadIdx.x; i < m; i += kNT) {
+      if (!kept[i]) continue;
+      int rank = 0;
+      for (int j = 0; j < m; ++j)
+        if (kept[j] && (keys[j] > keys[i] || (keys[j] == keys[i] && j < i))) ++rank;
+      out_idx[rank] = cand[i];
+    }
+  }
+  if (threadIdx.x == 0) out_count[0] = cnt;
+}
+
+// reconstruct_working_set for arbitrary (unsorted, duplicated) selections.
+__global__ void __launch_bounds__(kNT) working_set_kernel(const int32_t* selected, int n_sel,
+                                                          int n_pages, int window, int sinks,
+                                                          const int32_t* page_table,
+                                                          int32_t* out_pages, int8_t* out_prov,
+                                                          int32_t* out_phys, int32_t* out_len) {
+  extern __shared__ int8_t s_tag[];
+  __shared__ int s_scr[48];
+  for (int i = threadIdx.x; i < n_pages; i += kNT) s_tag[i] = CHESS_PROV_NONE;
+  __syncthreads();
+  for (int i = threadIdx.x; i < n_sel; i += kNT) {
+    const int p = selected[i];
+    if (p >= 0 && p < n_pages) s_tag[p] = CHESS_PROV_SEMANTIC;
+  }
+  __syncthreads();
+  for (int i = max(0, n_pages - window) + (int)threadIdx.x; i < n_pages; i += kNT)
+    s_tag[i] = CHESS_PROV_WINDOW;
+  __syncthreads();
+  for (int i = threadIdx.x; i < min(sinks, n_pages); i += kNT) s_tag[i] = CHESS_PROV_SINK;
+  __syncthreads();
+  int count = 0;
+  for (int base = 0; base < n_pages; base += kNT) {
+    const int i = base + threadIdx.x;
+    const int f = (i < n_pages && s_tag[i] != CHESS_PROV_NONE) ? 1 : 0;
+    int tot;
+    const int pos = block_exclusive_scan<kNT>(f, s_scr, &tot);
+    if (f) {
+      out_pages[count + pos] = i;
+      out_prov[count + pos] = s_tag[i];
+      if (out_phys) out_phys[count + pos] = page_table ? page_table[i] : i;
+    }
+    count += tot;
+  }
+  if (threadIdx.x == 0) *out_len = count;
+}
+
+__global__ void gather_pages_kernel(const int32_t* table, int n_pages, const int64_t* idx, int n,
+                                    int32_t* out, int32_t* err) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int64_t p = idx[i];
+  if (p < 0 || p >= n_pages) {
+    atomicMin(err, i + 1);
+    out[i] = -1;
+  } else {
+    out[i] = table[p];
+  }
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// launch wrappers
+// ---------------------------------------------------------------------------
+int launch_select(const ChessState& st, const Workspace& ws, const SelParams& prm, int grid,
+                  cudaStream_t stream) {
+  const size_t smem = (size_t)(st.d.batch + 1) * sizeof(int);
+  // persistent grid sized by occupancy (the scan keeps 64 KB of loads in
+  // flight per CTA; extra CTAs beyond residency would only serialise)
+  static int occ[2] = {0, 0};
+  const int ti = st.d.summary_dtype == 0 ? 0 : 1;
+  if (occ[ti] == 0) {
+    int o = 0;
+    if (ti == 0)
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, select_scan_kernel<float>, kNT, smem);
+    else
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, select_scan_kernel<double>, kNT, smem);
+    cudaGetLastError();
+    occ[ti] = o > 0 ? o : 1;
+  }
+  grid = occ[ti] * num_sms();
+  const int levels[3] = {0, 1, 2};
+  const int nlev = prm.full_scan ? 1 : 3;
+  for (int li = 0; li < nlev; ++li) {
+    const int level = prm.full_scan ? 3 : levels[li];
+    if (st.d.summary_dtype == 0)
+      select_scan_kernel<float><<<grid, kNT, smem, stream>>>(st, ws, prm, level);
+    else
+      select_scan_kernel<double><<<grid, kNT, smem, stream>>>(st, ws, prm, level);
+    const int rc = check_launch("select_scan");
+    if (rc) return rc;
+  }
+  return CHESS_OK;
+}
+
+int launch_build_ws_all(const ChessState& st, cudaStream_t stream);
+
+int launch_score_rows(const void* rows, int dtype, int64_t n, int64_t dim, int64_t ld,
+                      const double* anchor, double* scores, cudaStream_t stream) {
+  if (n == 0) return CHESS_OK;
+  if (dtype == CHESS_F64)
+    score_rows_kernel<double><<<(unsigned)n, 256, 0, stream>>>((const double*)rows, dim, ld, anchor, scores);
+  else if (dtype == CHESS_F32)
+    score_rows_kernel<float><<<(unsigned)n, 256, 0, stream>>>((const float*)rows, dim, ld, anchor, scores);
+  else
+    score_rows_kernel<__nv_bfloat16><<<(unsigned)n, 256, 0, stream>>>((const __nv_bfloat16*)rows, dim, ld, anchor, scores);
+  return check_launch("score_rows");
+}
+
+int launch_prune(const double* s_g, int G, const double* s_c, int C, const double* s_p, int P,
+                 const int64_t* p2c, const int64_t* c2g, double rg, double rc, double rp,
+                 int32_t* out_pages, int32_t* out_count, void* workspace, cudaStream_t stream) {
+  prune_kernel<<<1, kNT, 0, stream>>>(s_g, G, s_c, C, s_p, P, p2c, c2g, rg, rc, rp, out_pages,
+                                      out_count, (uint8_t*)workspace);
+  return check_launch("prune");
+}
+
+int launch_topk(const double* scores, int n, int k, const uint8_t* active, int32_t* out_idx,
+                int32_t* out_count, int sorted, void* workspace, cudaStream_t stream) {
+  topk_kernel<<<1, kNT, 0, stream>>>(scores, n, k, active, out_idx, out_count, sorted,
+                                     (uint8_t*)workspace);
+  return check_launch("topk");
+}
+
+int launch_working_set(const int32_t* selected, int n_sel, int n_pages, int window, int sinks,
+                       const int32_t* page_table, int32_t* out_pages, int8_t* out_prov,
+                       int32_t* out_phys, int32_t* out_len, cudaStream_t stream) {
+  const size_t smem = (size_t)n_pages + 16;
+  if (smem > 200 * 1024) return fail(CHESS_ERR_UNSUPPORTED, "working_set: %d pages too many", n_pages);
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(working_set_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  working_set_kernel<<<1, kNT, smem, stream>>>(selected, n_sel, n_pages, window, sinks, page_table,
+                                               out_pages, out_prov, out_phys, out_len);
+  return check_launch("working_set");
+}
+
+int launch_gather_pages(const int32_t* table, int n_pages, const int64_t* idx, int n, int32_t* out,
+                        int32_t* err, cudaStream_t stream) {
+  if (n == 0) return CHESS_OK;
+  gather_pages_kernel<<<(n + 255) / 256, 256, 0, stream>>>(table, n_pages, idx, n, out, err);
+  return check_launch("gather_pages");
+}
+
+namespace {
+__global__ void __launch_bounds__(256) build_ws_kernel(ChessState st) {
+  __shared__ int s_scr[64];
+  block_build_ws<256>(st, blockIdx.x, s_scr);
+}
+}  // namespace
+
+int launch_build_ws_all(const ChessState& st, cudaStream_t stream) {
+  build_ws_kernel<<<st.d.batch, 256, 0, stream>>>(st);
+  return check_launch("build_working_set");
+}
+
+}  // namespace chess

@@ -1,0 +1,172 @@
+"""Batched device decode engine: the per-token CHESS step on one stream.
+
+One decode token for every slot of the batch:
+
+    append (a1)  ->  L x sparse paged decode (K4)  ->  entropy + trigger (K5)
+                 ->  summary seal (K1, slots whose tail just sealed)
+                 ->  selection cascade (K2+K3, slots whose trigger fired)
+
+This is the device form of simulate.run_decode_loop's page loop
+(simulate.py:157-182) at token granularity: the trigger is evaluated when a
+generated page seals, reselection (backtracking) runs for the slots that
+fired, and the working set / block table is refreshed whenever the page
+table grows (selection.py:126-140).  Every stage is a C-ABI call; the whole
+step is capturable as one CUDA graph (no host sync inside).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+
+import torch
+
+from . import _lib
+from .config import SelectionConfig
+from .state import DecodeState
+
+
+def parse_policy(policy):
+    """('never'|'always'|'fixed'|'dynamic'|'every_step', interval) (simulate.py:78-91)."""
+    from .errors import ConfigurationError
+
+    if isinstance(policy, tuple):
+        return policy
+    if policy in ("dynamic", "never", "always", "every_step"):
+        return (policy, None)
+    if isinstance(policy, str) and policy.startswith("fixed(") and policy.endswith(")"):
+        interval = int(policy[6:-1])
+        if interval < 1:
+            raise ConfigurationError("fixed interval must be >= 1 page")
+        return ("fixed", interval)
+    raise ConfigurationError(
+        f"unknown policy {policy!r}; expected dynamic, never, always or fixed(N)"
+    )
+
+
+_POLICY_CODE = {
+    "never": _lib.POLICY_NEVER,
+    "always": _lib.POLICY_ALWAYS,
+    "fixed": _lib.POLICY_FIXED,
+    "dynamic": _lib.POLICY_DYNAMIC,
+    "every_step": _lib.POLICY_EVERY_STEP,
+}
+
+
+class ChessDecoder:
+    def __init__(
+        self,
+        state: DecodeState,
+        config: SelectionConfig,
+        policy="dynamic",
+        thresholds=None,
+        trigger_mode="joint",
+        full_scan=False,
+        softmax_scale=None,
+    ):
+        from .errors import ConfigurationError
+
+        self.state = state
+        self.config = config
+        s = state.shape
+        if config.page_size != s.page_size:
+            raise ConfigurationError("state and selection page sizes differ")
+        if (config.pages_per_chunk, config.chunks_per_grid) != (s.pages_per_chunk, s.chunks_per_grid):
+            raise ConfigurationError("state and selection fan-outs differ")
+        if config.window_pages != s.window_pages:
+            raise ConfigurationError("state and selection window differ")
+        kind, interval = parse_policy(policy)
+        if kind == "dynamic" and thresholds is None:
+            raise ConfigurationError("policy 'dynamic' needs calibrated thresholds")
+        if trigger_mode not in ("joint", "any"):
+            raise ValueError(f"unknown trigger mode {trigger_mode!r}")
+        self.kind = kind
+        self.sel_cfg = _lib.ChessSelectCfg(
+            config.rho_grid, config.rho_chunk, config.rho_page, 1 if full_scan else 0, 0
+        )
+        self.sel_cfg_all = _lib.ChessSelectCfg(
+            config.rho_grid, config.rho_chunk, config.rho_page, 1 if full_scan else 0, 1
+        )
+        self.trig_cfg = _lib.ChessTriggerCfg()
+        self.trig_cfg.policy = _POLICY_CODE[kind]
+        self.trig_cfg.interval = interval or 1
+        self.trig_cfg.mode = 0 if trigger_mode == "joint" else 1
+        if thresholds is not None:
+            self.trig_cfg.tau_entropy = thresholds.tau_entropy
+            self.trig_cfg.tau_varentropy = thresholds.tau_varentropy
+        self.scale = softmax_scale if softmax_scale is not None else 1.0 / math.sqrt(s.head_dim)
+        self.graph = None
+
+    # ------------------------------------------------------------------
+    # prefill: KV rows already in the pool, page tables/counters set
+    # ------------------------------------------------------------------
+    def build_index(self, n_pages: torch.Tensor, stream=None):
+        """K1b: index pages [0, n_pages[s]) of every slot (prefill)."""
+        _lib.call("chess_summary_build", self.state.ref, _lib.ptr(n_pages), _lib.stream_ptr(stream))
+
+    def select(self, force_all=False, stream=None):
+        cfg = self.sel_cfg_all if force_all else self.sel_cfg
+        _lib.call("chess_select", self.state.ref, C.byref(cfg), _lib.stream_ptr(stream))
+
+    def initial_selection(self, stream=None):
+        """Post-prefill selection (simulate.py:147-151); 'never' keeps every page."""
+        if self.kind == "never":
+            st = self.state
+            n = st.num_sealed
+            ar = torch.arange(st.shape.max_pages, device=st.device, dtype=torch.int32)
+            st.semantic.copy_(ar.unsqueeze(0).expand_as(st.semantic))
+            st.n_semantic.copy_(n)
+            _lib.call("chess_build_working_set", st.ref, _lib.stream_ptr(stream))
+        else:
+            self.select(force_all=True, stream=stream)
+
+    # ------------------------------------------------------------------
+    # one decode token for the whole batch
+    # ------------------------------------------------------------------
+    def append(self, k_new, v_new, stream=None):
+        _lib.call(
+            "chess_append_kv", self.state.ref, _lib.ptr(k_new), _lib.ptr(v_new),
+            k_new.stride(0), None, _lib.stream_ptr(stream),
+        )
+
+    def attend(self, layer, q, out, lse=None, stream=None):
+        """K4 for one layer: q/out [batch, q_heads, head_dim] (batch stride may be padded)."""
+        _lib.call(
+            "chess_sparse_decode", self.state.ref, layer, _lib.ptr(q), q.stride(0),
+            _lib.ptr(out), out.stride(0), _lib.ptr(lse), self.scale, _lib.stream_ptr(stream),
+        )
+
+    def entropy_trigger(self, logits, entropy_out=None, stream=None):
+        _lib.call(
+            "chess_entropy_trigger", self.state.ref, _lib.ptr(logits), logits.shape[1],
+            logits.stride(0), C.byref(self.trig_cfg), _lib.ptr(entropy_out),
+            _lib.stream_ptr(stream),
+        )
+
+    def seal(self, stream=None):
+        _lib.call("chess_summary_seal", self.state.ref, _lib.stream_ptr(stream))
+
+    def step(self, k_new, v_new, q, logits, out, lse=None, entropy_out=None, stream=None):
+        """k_new/v_new [b, D] bf16; q/out [b, L, H_q, d] bf16; logits [b, V] f32;
+        lse (optional) f32 [L, b, H_q]."""
+        self.append(k_new, v_new, stream)
+        for layer in range(self.state.shape.layers):
+            self.attend(layer, q[:, layer], out[:, layer],
+                        None if lse is None else lse[layer], stream)
+        self.entropy_trigger(logits, entropy_out, stream)
+        self.seal(stream)
+        if self.kind != "never":
+            self.select(force_all=False, stream=stream)
+
+    # ------------------------------------------------------------------
+    def capture(self, k_new, v_new, q, logits, out, lse=None, entropy_out=None):
+        """Capture `step` on static buffers as one CUDA graph."""
+        g = torch.cuda.CUDAGraph()
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            with torch.cuda.graph(g, stream=s):
+                self.step(k_new, v_new, q, logits, out, lse, entropy_out, stream=s)
+        torch.cuda.current_stream().wait_stream(s)
+        self.graph = g
+        return g

@@ -1,0 +1,139 @@
+"""Device-resident batched decode state (the buffers behind a ChessState).
+
+Every buffer is a torch CUDA tensor owned here; the C-ABI struct only holds
+their addresses (include/chess_b200.h: "the caller owns all device buffers").
+Layouts are documented in the header and DESIGN.md §"Data layout in HBM".
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass
+
+import torch
+
+from . import _lib
+
+
+def _round_up(x: int, m: int) -> int:
+    return (x + m - 1) // m * m
+
+
+@dataclass(frozen=True)
+class Shape:
+    batch: int
+    layers: int
+    kv_heads: int
+    q_heads: int
+    head_dim: int
+    page_size: int
+    pages_per_chunk: int
+    chunks_per_grid: int
+    max_pages: int
+    window_pages: int
+    max_ws: int
+    n_phys: int
+    summary_dtype: str = "f32"  # "f32" mirrors scanned, or "f64"
+
+    @property
+    def dim(self) -> int:
+        return self.layers * self.kv_heads * self.head_dim
+
+    @property
+    def ld(self) -> int:
+        return _round_up(self.dim, 4)
+
+    @property
+    def max_chunks(self) -> int:
+        return math.ceil(self.max_pages / self.pages_per_chunk)
+
+    @property
+    def max_grids(self) -> int:
+        return math.ceil(self.max_chunks / self.chunks_per_grid)
+
+
+class DecodeState:
+    """Allocates and owns every buffer of a ChessState for `shape`."""
+
+    def __init__(self, shape: Shape, device="cuda", kv_pool=None):
+        self.shape = s = shape
+        self.device = torch.device(device)
+        dev = self.device
+        b, ld = s.batch, s.ld
+        i32 = dict(dtype=torch.int32, device=dev)
+        f64 = dict(dtype=torch.float64, device=dev)
+        f32 = dict(dtype=torch.float32, device=dev)
+        u8 = dict(dtype=torch.uint8, device=dev)
+        if kv_pool is None:
+            kv_shape = (s.layers, s.n_phys, s.kv_heads, s.page_size, s.head_dim)
+            self.k_pool = torch.empty(kv_shape, dtype=torch.bfloat16, device=dev)
+            self.v_pool = torch.empty(kv_shape, dtype=torch.bfloat16, device=dev)
+        else:
+            self.k_pool, self.v_pool = kv_pool
+        self.page_table = torch.zeros((b, s.max_pages), **i32)
+        self.num_pages = torch.zeros(b, **i32)
+        self.tail_fill = torch.zeros(b, **i32)
+        self.token_count = torch.zeros(b, dtype=torch.int64, device=dev)
+        self.sink_count = torch.zeros(b, **i32)
+        self.sealed = torch.zeros(b, **u8)
+        self.num_sealed = torch.zeros(b, **i32)
+        self.page_vec64 = torch.zeros((b, s.max_pages, ld), **f64)
+        self.chunk_sum64 = torch.zeros((b, s.max_chunks, ld), **f64)
+        self.grid_sum64 = torch.zeros((b, s.max_grids, ld), **f64)
+        self.chunk_vec64 = torch.zeros((b, s.max_chunks, ld), **f64)
+        self.grid_vec64 = torch.zeros((b, s.max_grids, ld), **f64)
+        if s.summary_dtype == "f32":
+            self.page_vec32 = torch.zeros((b, s.max_pages, ld), **f32)
+            self.chunk_vec32 = torch.zeros((b, s.max_chunks, ld), **f32)
+            self.grid_vec32 = torch.zeros((b, s.max_grids, ld), **f32)
+        else:
+            self.page_vec32 = self.chunk_vec32 = self.grid_vec32 = None
+        self.key_sum = torch.zeros((b, ld), **f64)
+        self.anchor = torch.zeros((b, ld), **f64)
+        self.semantic = torch.zeros((b, s.max_pages), **i32)
+        self.n_semantic = torch.zeros(b, **i32)
+        self.sel_stats = torch.zeros((b, 8), **i32)
+        self.ws_logical = torch.zeros((b, s.max_ws), **i32)
+        self.block_table = torch.zeros((b, s.max_ws), **i32)
+        self.ws_prov = torch.zeros((b, s.max_ws), dtype=torch.int8, device=dev)
+        self.ws_len = torch.zeros(b, **i32)
+        self.ent_ring = torch.zeros((b, s.page_size), **f64)
+        self.ent_count = torch.zeros(b, **i32)
+        self.gen_pages = torch.zeros(b, **i32)
+        self.page_stats = torch.zeros((b, 2), **f64)
+        self.fire = torch.zeros(b, **u8)
+
+        self.c = _lib.ChessState()
+        d = self.c.d
+        d.batch, d.layers, d.kv_heads, d.q_heads = b, s.layers, s.kv_heads, s.q_heads
+        d.head_dim, d.page_size = s.head_dim, s.page_size
+        d.pages_per_chunk, d.chunks_per_grid = s.pages_per_chunk, s.chunks_per_grid
+        d.max_pages, d.window_pages, d.max_ws = s.max_pages, s.window_pages, s.max_ws
+        d.summary_dtype = 0 if s.summary_dtype == "f32" else 1
+        d.dim, d.ld, d.n_phys = s.dim, ld, s.n_phys
+        lib = _lib.load()
+        _lib.check(lib.chess_validate_dims(C.byref(d)), "validate_dims")
+        nbytes = lib.chess_workspace_bytes(C.byref(d))
+        self.workspace = torch.zeros(nbytes, dtype=torch.uint8, device=dev)
+        for name in _lib.STATE_POINTERS:
+            setattr(self.c, name, _lib.ptr(getattr(self, name)))
+        self.c.workspace_bytes = nbytes
+        self.ref = C.byref(self.c)
+
+    # ------------------------------------------------------------------
+    def reset(self, mask=None, stream=None):
+        _lib.call("chess_reset_slots", self.ref, _lib.ptr(mask), _lib.stream_ptr(stream))
+
+    def scan_matrices(self):
+        """(grid, chunk, page) matrices the selection scan reads."""
+        if self.shape.summary_dtype == "f32":
+            return self.grid_vec32, self.chunk_vec32, self.page_vec32
+        return self.grid_vec64, self.chunk_vec64, self.page_vec64
+
+    def bytes_allocated(self) -> int:
+        tot = 0
+        for v in self.__dict__.values():
+            if isinstance(v, torch.Tensor):
+                tot += v.numel() * v.element_size()
+        return tot

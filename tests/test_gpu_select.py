@@ -1,0 +1,164 @@
+"""K2+K3 parity: anchor scoring + masked top-k cascade + working set + block
+table vs the oracle (selection.py:44-140, kv_store.py:156-166).
+
+Bar: index sets identical; block tables bit-exact given
+identical selections.  f64 scan: exact.  f32 scan: exact against the oracle
+fed the same f32 summaries (kernel-isolated), and against the f64 oracle up
+to certified near-ties (end-to-end).
+"""
+
+import math
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import pagesel_ref as ref
+from paper_2602_20732_b200 import _lib
+from paper_2602_20732_b200.config import SelectionConfig, preset_config
+
+pytestmark = pytest.mark.gpu
+
+
+def _select(st, force_all=True, full_scan=False, cfg=None):
+    sc = _lib.ChessSelectCfg(cfg.rho_grid, cfg.rho_chunk, cfg.rho_page, int(full_scan), int(force_all))
+    import ctypes
+
+    _lib.call("chess_select", st.ref, ctypes.byref(sc), _lib.stream_ptr())
+    torch.cuda.synchronize()
+
+
+def _oracle_on(h: ref.Hierarchy, cfg, mats=None):
+    """Cascade on the f64 hierarchy, or on given (grid, chunk, page) matrices."""
+    a, _ = ref.anchor(h.page_vectors, cfg.window_pages)
+    G, Cn, P = h.counts
+    if mats is None:
+        mats = (h.grid_vectors, h.chunk_vectors, h.page_vectors)
+    s = [m @ a for m in mats]
+    p2c, c2g = h.parent_maps()
+    sel, info = ref.prune(s[0], s[1], s[2], p2c, c2g, cfg.ratios)
+    return sel, info, s
+
+
+def _instances(rng, n):
+    for t in range(n):
+        P = int(rng.integers(1, 700))
+        dim = int(rng.choice([8, 16, 40, 128, 300, 1024, 2052]))
+        nc = int(rng.integers(1, 10))
+        ng = int(rng.integers(1, 10))
+        rhos = [float(rng.choice([1.0, 0.5, 0.2, 0.1, float(rng.uniform(0.05, 1.0))])) for _ in range(3)]
+        cfg = SelectionConfig(
+            pages_per_chunk=nc, chunks_per_grid=ng, rho_grid=rhos[0], rho_chunk=rhos[1],
+            rho_page=rhos[2], window_pages=int(rng.integers(1, 9)), sink_pages=int(rng.integers(0, 4)),
+        )
+        yield P, dim, cfg
+
+
+@pytest.mark.parametrize("full_scan", [False, True])
+def test_select_f64_exact(full_scan):
+    from helpers import index_state, load_vectors, read_selection, set_tables
+
+    rng = np.random.default_rng(11)
+    for P, dim, cfg in _instances(rng, 25):
+        st = index_state(3, dim, 720, cfg, summary_dtype="f64")
+        hs = []
+        for slot in range(3):
+            n = max(1, P - 37 * slot)
+            rows = rng.standard_normal((n, dim))
+            load_vectors(st, slot, rows)
+            set_tables(st, slot, n + slot, cfg.sink_pages)  # page table may hold an open tail
+            hs.append((ref.Hierarchy.from_rows(rows, cfg.pages_per_chunk, cfg.chunks_per_grid), n))
+        _select(st, full_scan=full_scan, cfg=cfg)
+        for slot, (h, n) in enumerate(hs):
+            sel, info, _ = _oracle_on(h, cfg)
+            sem, ws, bt, prov = read_selection(st, slot)
+            np.testing.assert_array_equal(sem, sel, err_msg=f"P={n} dim={dim} cfg={cfg}")
+            pages, pv = ref.working_set(sel, n + slot, cfg.window_pages, cfg.sink_pages)
+            np.testing.assert_array_equal(ws, pages)
+            table = st.page_table[slot, : n + slot].cpu().numpy()
+            np.testing.assert_array_equal(bt, ref.gather(list(table), pages))
+            names = {1: "semantic", 2: "window", 3: "sink"}
+            assert [names[int(x)] for x in prov] == [pv[p] for p in pages]
+            stats = st.sel_stats[slot].cpu().numpy()
+            G, C, Pn = h.counts
+            assert tuple(stats[:3]) == (G, C, Pn)
+            assert stats[3] == info["active_c"] and stats[4] == info["active_p"]
+
+
+def test_select_f32_kernel_isolated_and_end_to_end():
+    from helpers import index_state, load_vectors, read_selection, set_tables
+
+    rng = np.random.default_rng(5)
+    flips = 0
+    for P, dim, cfg in _instances(rng, 30):
+        st = index_state(2, dim, 720, cfg, summary_dtype="f32")
+        hs = []
+        for slot in range(2):
+            rows = rng.standard_normal((P, dim))
+            load_vectors(st, slot, rows)
+            set_tables(st, slot, P, cfg.sink_pages)
+            hs.append(ref.Hierarchy.from_rows(rows, cfg.pages_per_chunk, cfg.chunks_per_grid))
+        _select(st, cfg=cfg)
+        for slot, h in enumerate(hs):
+            G, C, Pn = h.counts
+            mats = (
+                st.grid_vec32[slot, :G, :dim].double().cpu().numpy(),
+                st.chunk_vec32[slot, :C, :dim].double().cpu().numpy(),
+                st.page_vec32[slot, :Pn, :dim].double().cpu().numpy(),
+            )
+            # the f32 mirrors are the correctly rounded f64 centroids
+            np.testing.assert_array_equal(mats[0], h.grid_vectors.astype(np.float32).astype(np.float64))
+            np.testing.assert_array_equal(mats[1], h.chunk_vectors.astype(np.float32).astype(np.float64))
+            sem = read_selection(st, slot)[0]
+            sel_iso, _, _ = _oracle_on(h, cfg, mats)
+            np.testing.assert_array_equal(sem, sel_iso)  # (B) kernel-isolated: exact
+            sel64, info, s64 = _oracle_on(h, cfg)
+            if not np.array_equal(sem, sel64):  # (A) end-to-end: certified near-tie only
+                flips += 1
+                a, _ = ref.anchor(h.page_vectors, cfg.window_pages)
+                eps = (math.ceil(math.log2(dim)) + 4) * 2.0**-24
+                gaps = []
+                for lvl, (mat64, mat32) in enumerate(zip((h.grid_vectors, h.chunk_vectors, h.page_vectors), mats)):
+                    bound = eps * (np.abs(mat64) @ np.abs(a))
+                    gaps.append(np.max(np.abs(mat64 @ a - mat32 @ a) - bound))
+                assert max(gaps) <= 0, "score error exceeds the certified bound"
+    assert flips <= 2
+
+
+def test_select_aggressive_budget_2048():
+    """Acceptance C1 shape (test_acceptance.py:45-65) on the device."""
+    from helpers import index_state, load_vectors, read_selection, set_tables
+
+    rng = np.random.default_rng(0)
+    rows = rng.standard_normal((2048, 32))
+    a_dummy = rng.standard_normal(32)  # consumes the same RNG stream as the reference test
+    del a_dummy
+    for name in ("aggressive", "moderate", "conservative"):
+        cfg = preset_config(name)
+        st = index_state(1, 32, 2048, cfg, summary_dtype="f64")
+        load_vectors(st, 0, rows)
+        set_tables(st, 0, 2048, cfg.sink_pages)
+        _select(st, cfg=cfg)
+        sem = read_selection(st, 0)[0]
+        h = ref.Hierarchy.from_rows(rows, 8, 8)
+        sel, _, _ = _oracle_on(h, cfg)
+        np.testing.assert_array_equal(sem, sel)
+
+
+def test_select_gated_by_fire_and_empty():
+    from helpers import index_state, load_vectors, read_selection, set_tables
+
+    cfg = preset_config("aggressive", pages_per_chunk=2, chunks_per_grid=2)
+    st = index_state(3, 16, 64, cfg, summary_dtype="f32")
+    rng = np.random.default_rng(3)
+    load_vectors(st, 0, rng.standard_normal((20, 16)))
+    set_tables(st, 0, 20, 1)
+    load_vectors(st, 1, rng.standard_normal((20, 16)))
+    set_tables(st, 1, 20, 1)
+    set_tables(st, 2, 0, 1)  # empty slot
+    st.fire.copy_(torch.tensor([1, 0, 1], dtype=torch.uint8))
+    st.n_semantic[1] = 0
+    _select(st, force_all=False, cfg=cfg)
+    assert int(st.n_semantic[0]) > 0
+    assert int(st.n_semantic[1]) == 0 and int(st.ws_len[1]) == 0  # not fired: untouched
+    assert int(st.n_semantic[2]) == 0 and int(st.ws_len[2]) == 0
