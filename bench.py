@@ -1,0 +1,466 @@
+"""CHESS decode hot-path benchmark (BASELINE.json metric: decode tokens/s and
+us/step (select+attn) at 1% KV; % HBM roofline).
+
+A step = one decode token for every sequence of the batch through the
+device engine: KV append -> L x sparse paged decode -> entropy + trigger ->
+summary seal -> selection cascade.  Headline variant: selection forced on
+every step (worst case); the dynamic (backtracking) and
+attention-only variants are reported alongside.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg3]
+  python bench.py --impl reference ...   # reference CPU path (oracle port)
+
+N>1 (torchrun): batch-sharded replicas, each rank owns `batch` sequences
+(weak scaling, no data-path collective); time = max over ranks.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import sys
+import threading
+import time
+from pathlib import Path
+
+REPO = Path(__file__).resolve().parent
+sys.path.insert(0, str(REPO))
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+
+def _dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+# ---------------------------------------------------------------------------
+# clocks (NVML, the library behind nvidia-smi) sampled during the timed region
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    REASONS = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+        0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+        0x80: "hw_power_brake_slowdown", 0x100: "display_clocks_setting",
+    }
+
+    def __init__(self, index=0, period=0.01):
+        self.samples, self.reasons = [], set()
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self.period = period
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:  # pragma: no cover - no NVML
+            self.nv = None
+
+    def _run(self):
+        nv = self.nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.nv:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.nv:
+            self.t.join()
+
+    def summary(self):
+        med = float(np.median(self.samples)) if self.samples else None
+        return {"sm_mhz": med, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------------------
+# GPU arm
+# ---------------------------------------------------------------------------
+def run_gpu(args):
+    import torch.distributed as dist
+
+    from paper_2602_20732_b200 import _lib
+    from paper_2602_20732_b200.config import preset_config
+    from paper_2602_20732_b200.engine import ChessDecoder
+    from paper_2602_20732_b200.synthetic import CONFIGS, DESCRIPTIONS, SyntheticDecode
+
+    rank, world, local = _dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    _lib.load()
+    peaks = json.loads((REPO / "MEASURED_PEAKS.json").read_text()) if (REPO / "MEASURED_PEAKS.json").exists() else {}
+    hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    peak_src = "measured" if "hbm_gbs" in peaks else "fallback"
+
+    cfg_name = args.config
+    c = CONFIGS[cfg_name]
+    batch = c["batch"] if args.batch is None else args.batch
+    # cfg4 is batch-sharded: total batch split across ranks; others replicate per rank
+    if cfg_name == "cfg4" and args.batch is None:
+        batch = max(1, c["batch"] // world)
+    total_steps = args.warmup + args.steps
+    ring = 64 if c["page"] == 32 else 32
+    gen_pages = math.ceil((total_steps + 2 * ring + 64) / c["page"]) + 4
+    wl = SyntheticDecode(cfg_name, batch=batch, gen_pages=gen_pages, ring=ring, seed=rank,
+                         summary_dtype=args.summary_dtype)
+    st = wl.st
+    sh = wl.shape
+    sel = preset_config("aggressive", page_size=sh.page_size)
+    P, B, L = wl.P, wl.B, sh.layers
+
+    def fresh_decoder(policy, thresholds=None):
+        st.reset()
+        st.num_pages.fill_(P)
+        st.tail_fill.fill_(B)
+        st.token_count.fill_(P * B)
+        st.sink_count.fill_(1)
+        dec = ChessDecoder(st, sel, policy=policy, thresholds=thresholds, full_scan=args.full_scan)
+        wl.prefill(dec)
+        # one eager step: first-call attribute/occupancy setup happens outside capture
+        k, v, q, lg = wl.step_inputs(ring - 1)
+        dec.step(k, v, q, lg, wl.out)
+        torch.cuda.synchronize()
+        return dec
+
+    def capture_ring(dec):
+        graphs = []
+        for r in range(ring):
+            k, v, q, lg = wl.step_inputs(r)
+            graphs.append(dec.capture(k, v, q, lg, wl.out))
+        return graphs
+
+    def timed(dec, graphs, steps, warmup, sample_clocks=False):
+        # eager warm-up of every kernel path before capture happened in capture_ring;
+        for t in range(warmup):
+            graphs[t % ring].replay()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        sampler = ClockSampler(local) if sample_clocks else None
+        ws_before = st.ws_len.float().mean().item()
+        stats_before = st.sel_stats.clone()
+        fill0 = int(st.tail_fill[0].item())
+        torch.cuda.synchronize()
+        if sampler:
+            sampler.__enter__()
+        t0.record()
+        for t in range(steps):
+            graphs[(warmup + t) % ring].replay()
+        t1.record()
+        torch.cuda.synchronize()
+        if sampler:
+            sampler.__exit__()
+        if world > 1:
+            dist.barrier()
+        ms = t0.elapsed_time(t1)
+        if world > 1:
+            tt = torch.tensor([ms], device="cuda")
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            ms = tt.item()
+        ws_after = st.ws_len.float().mean().item()
+        fills = [((fill0 + t) % B) + 1 for t in range(steps)]
+        return {
+            "ms": ms,
+            "ws_mean": 0.5 * (ws_before + ws_after),
+            "mean_fill": float(np.mean(fills)),
+            "sel_stats": st.sel_stats.cpu().numpy(),
+            "triggers": int(st.gen_pages.sum().item()),
+            "clocks": sampler.summary() if sampler else None,
+        }
+
+    def attn_bytes_per_layer(ws_mean, mean_fill):
+        kv_rows = ws_mean * B - (B - mean_fill)
+        kv = batch * kv_rows * 2 * sh.kv_heads * sh.head_dim * 2
+        qo = batch * sh.q_heads * sh.head_dim * 2 * 2
+        return kv + qo
+
+    def select_bytes(stats):
+        # rows actually scanned: G + A_c + A_p per sequence, f32/f64 rows; + anchor
+        es = 4 if args.summary_dtype == "f32" else 8
+        rows = stats[:, 0] + stats[:, 3] + stats[:, 4] if not args.full_scan else stats[:, 0] + stats[:, 1] + stats[:, 2]
+        return float(np.sum(rows) * sh.dim * es + batch * sh.dim * 8)
+
+    def step_bytes(res, select_every):
+        a = L * attn_bytes_per_layer(res["ws_mean"], res["mean_fill"])
+        e = batch * wl.vocab * 4
+        app = batch * sh.dim * (2 * 2 + 2 * 8)
+        s = select_bytes(res["sel_stats"]) if select_every else 0.0
+        return a + e + app + s
+
+    results = {}
+    # ---- headline: selection forced every step ----
+    dec = fresh_decoder("every_step")
+    graphs = capture_ring(dec)
+    res = timed(dec, graphs, args.steps, args.warmup, sample_clocks=True)
+    results["select_every_step"] = res
+
+    # ---- kernel-level timing (CUDA events on the launching stream) ----
+    stream = torch.cuda.current_stream()
+    k, v, q, lg = wl.step_inputs(0)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+    reps = 5
+    torch.cuda.synchronize()
+    ev[0].record(stream)
+    for _ in range(reps):
+        for layer in range(L):
+            dec.attend(layer, q[:, layer], wl.out[:, layer])
+    ev[1].record(stream)
+    for _ in range(reps):
+        dec.select(force_all=True)
+    ev[2].record(stream)
+    torch.cuda.synchronize()
+    attn_launch_s = ev[0].elapsed_time(ev[1]) / 1e3 / (reps * L)
+    select_call_s = ev[1].elapsed_time(ev[2]) / 1e3 / reps
+    ws_now = st.ws_len.float().mean().item()
+    fill_now = float(st.tail_fill.float().mean().item())
+    attn_launch_bytes = attn_bytes_per_layer(ws_now, fill_now)
+    sel_call_bytes = select_bytes(st.sel_stats.cpu().numpy())
+
+    # ---- e2e through the C-ABI with host buffers (pinned), headline variant ----
+    hk = [t.cpu().pin_memory() for t in (wl.k_ring[0], wl.v_ring[0], wl.q_ring[0], wl.logit_ring[0])]
+    h_out = torch.empty(wl.out.shape, dtype=wl.out.dtype).pin_memory()
+    dec = fresh_decoder("every_step")
+    graphs = capture_ring(dec)
+    for t in range(args.warmup):
+        graphs[t % ring].replay()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for t in range(args.steps):
+        r = (args.warmup + t) % ring
+        wl.k_ring[r].copy_(hk[0], non_blocking=True)
+        wl.v_ring[r].copy_(hk[1], non_blocking=True)
+        wl.q_ring[r].copy_(hk[2], non_blocking=True)
+        wl.logit_ring[r].copy_(hk[3], non_blocking=True)
+        graphs[r].replay()
+        h_out.copy_(wl.out, non_blocking=True)
+    e1.record()
+    torch.cuda.synchronize()
+    e2e_ms = e0.elapsed_time(e1)
+    if world > 1:
+        tt = torch.tensor([e2e_ms], device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_ms = tt.item()
+    h2d = sum(t.numel() * t.element_size() for t in hk)
+    d2h = h_out.numel() * h_out.element_size()
+
+    # ---- amortised dynamic (backtracking) and attention-only variants ----
+    if not args.headline_only:
+        dec = fresh_decoder("dynamic", wl.tau)
+        graphs = capture_ring(dec)
+        results["dynamic"] = timed(dec, graphs, args.steps, args.warmup)
+        dec = fresh_decoder("fixed(1000000)")
+        graphs = capture_ring(dec)
+        results["attn_only"] = timed(dec, graphs, args.steps, args.warmup)
+    del graphs
+
+    head = results["select_every_step"]
+    ms_step = head["ms"] / args.steps
+    value = world * batch / (ms_step / 1e3)
+    bytes_step = step_bytes(head, True)
+    achieved = attn_launch_bytes / attn_launch_s / 1e9
+    out = {
+        "metric": "decode tokens/s (select+attn every step) at 1% KV",
+        "value": value,
+        "unit": "tokens/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms_step,
+        "us_per_step": ms_step * 1e3,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "bf16 KV / f32 summaries / f64 scores",
+        "data": "synthetic (planted-relevance keys, random-init shapes)",
+        "config": {
+            "workload": f"{cfg_name}: {DESCRIPTIONS[cfg_name]}",
+            "batch_per_gpu": batch,
+            "context": c["ctx"],
+            "page_size": B,
+            "preset": "aggressive (0.5, 0.2, 0.1), W=4, sinks=1",
+            "parallelism": f"batch-shard x{world}" if world > 1 else "single GPU",
+            "summary_dtype": args.summary_dtype,
+            "scan": "full (Alg.1 literal)" if args.full_scan else "conditional (output-identical)",
+            "kv_pool_pages": sh.n_phys,
+            "kv_aliased": wl.aliased,
+            "l2": "inputs larger than L2 (step reads >> 126 MB)",
+            "ws_pages_mean": head["ws_mean"],
+        },
+        "bytes_per_step": bytes_step,
+        "step_roofline": {"achieved": bytes_step / (ms_step / 1e3) / 1e9, "peak": hbm_peak, "unit": "GB/s",
+                          "frac": bytes_step / (ms_step / 1e3) / 1e9 / hbm_peak},
+        "roofline": {
+            "kernel": "sparse_decode (K4)",
+            "bound": "hbm",
+            "achieved": achieved,
+            "peak": hbm_peak,
+            "peak_source": peak_src,
+            "unit": "GB/s",
+            "frac": achieved / hbm_peak,
+            "traffic": None,
+            "bytes_per_launch": attn_launch_bytes,
+            "launch_us": attn_launch_s * 1e6,
+        },
+        "select_roofline": {
+            "kernel": "select cascade (K2+K3, 3 launches)",
+            "achieved": sel_call_bytes / select_call_s / 1e9,
+            "peak": hbm_peak, "unit": "GB/s",
+            "frac": sel_call_bytes / select_call_s / 1e9 / hbm_peak,
+            "bytes_per_call": sel_call_bytes, "call_us": select_call_s * 1e6,
+        },
+        "e2e": {
+            "value": world * batch * args.steps / (e2e_ms / 1e3),
+            "unit": "tokens/s",
+            "h2d_bytes_per_step": h2d,
+            "d2h_bytes_per_step": d2h,
+        },
+        "gpu_launches": args.steps * (L + 6),
+        "clocks": head["clocks"],
+    }
+    if not args.headline_only:
+        out["variants"] = {
+            name: {"us_per_step": r["ms"] / args.steps * 1e3,
+                   "tokens_per_s": world * batch / (r["ms"] / args.steps / 1e3),
+                   "ws_pages_mean": r["ws_mean"]}
+            for name, r in results.items()
+        }
+        out["variants"]["dynamic"]["generated_pages_sealed"] = results["dynamic"]["triggers"]
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_baseline(cfg_name, steps=1)
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+# ---------------------------------------------------------------------------
+# CPU arms: the oracle port of the reference timed on the host cores
+# ---------------------------------------------------------------------------
+def _cpu_sample_setup(cfg_name, seed=0):
+    from oracle import pagesel_ref as ref
+    from paper_2602_20732_b200.config import preset_config
+    from paper_2602_20732_b200.synthetic import CONFIGS
+
+    c = CONFIGS[cfg_name]
+    B, P = c["page"], c["ctx"] // c["page"]
+    L, H, Hq, d = c["layers"], c["kv_heads"], c["q_heads"], c["head_dim"]
+    D = L * H * d
+    rng = np.random.default_rng(seed)
+    cfg = preset_config("aggressive", page_size=B)
+    rows = rng.standard_normal((P, D)) / math.sqrt(D)
+    h = ref.Hierarchy.from_rows(rows, cfg.pages_per_chunk, cfg.chunks_per_grid)
+    kv_pages = 64  # physical pages backing the sample's working set
+    k_pool = rng.standard_normal((kv_pages, H, B, d)).astype(np.float32)
+    v_pool = rng.standard_normal((kv_pages, H, B, d)).astype(np.float32)
+    q = rng.standard_normal((L, Hq, d)).astype(np.float32)
+    logits = rng.standard_normal(c["vocab"]).astype(np.float32)
+    return ref, cfg, h, k_pool, v_pool, q, logits, (L, H, Hq, d, B, P)
+
+
+def _cpu_step(ref, cfg, h, k_pool, v_pool, q, logits, dims):
+    from oracle import attention as attn
+
+    L, H, Hq, d, B, P = dims
+    sel, _ = ref.select_for_index(h, cfg)
+    pages, _ = ref.working_set(sel, P, cfg.window_pages, cfg.sink_pages)
+    bt = np.asarray([[i % k_pool.shape[0] for i in range(len(pages))]])
+    for layer in range(L):
+        attn.sparse_decode(q[None, layer], k_pool, v_pool, bt, [len(pages)], [B], 1.0 / math.sqrt(d))
+    ref.entropy_from_logits(logits)
+    return len(pages)
+
+
+def cpu_baseline(cfg_name, steps=1):
+    setup = _cpu_sample_setup(cfg_name)
+    t = time.perf_counter()
+    for _ in range(steps):
+        _cpu_step(*setup)
+    dt = (time.perf_counter() - t) / steps
+    return {
+        "value": 1.0 / dt,
+        "unit": "tokens/s",
+        "cores": os.cpu_count(),
+        "kind": "port",
+        "sample": f"1 sequence x 1 decode step of {cfg_name} (selection over the full index + "
+                  f"{setup[-1][0]}-layer attention restatement + entropy), oracle/ NumPy port, "
+                  f"all host threads (BLAS)",
+        "seconds_per_token": dt,
+    }
+
+
+def run_reference(args):
+    rank, world, _ = _dist_env()
+    if rank != 0:
+        return
+    from paper_2602_20732_b200.synthetic import DESCRIPTIONS
+
+    setup = _cpu_sample_setup(args.config)
+    for _ in range(min(args.warmup, 1)):
+        _cpu_step(*setup)
+    t = time.perf_counter()
+    for _ in range(args.steps):
+        _cpu_step(*setup)
+    dt = (time.perf_counter() - t) / args.steps
+    v = 1.0 / dt
+    sample = (f"each step = 1 sequence x 1 decode token of {args.config} (oracle NumPy port of "
+              f"pagesel selection + attention restatement + entropy)")
+    print(json.dumps({
+        "impl": "reference",
+        "metric": "decode tokens/s (select+attn every step) at 1% KV",
+        "value": v, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{args.config}: {DESCRIPTIONS[args.config]}"},
+        "cpu_baseline": {"value": v, "unit": "tokens/s", "cores": os.cpu_count(), "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="chess", choices=["chess", "reference"])
+    ap.add_argument("--config", default="cfg3")
+    ap.add_argument("--batch", type=int, default=None)
+    ap.add_argument("--summary-dtype", default="f32", choices=["f32", "f64"])
+    ap.add_argument("--full-scan", action="store_true")
+    ap.add_argument("--headline-only", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_gpu(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -90,7 +90,7 @@ size_t workspace_layout(const ChessDims& d, void* base, Workspace* ws) {
   const int64_t mr = max_rows(d);
   const int64_t nsl = (d.ld + kScanSlice - 1) / kScanSlice;
   const int64_t gq = d.kv_heads > 0 ? d.q_heads / d.kv_heads : 1;
-  const int64_t attn_slots = b * d.kv_heads + kAttnCtasMax;
+  const int64_t attn_slots = b * d.kv_heads + kAttnWarpsMax;
   size_t off = 0;
   auto take = [&](size_t bytes) {
     const size_t o = off;
@@ -106,7 +106,7 @@ size_t workspace_layout(const ChessDims& d, void* base, Workspace* ws) {
   const size_t o_kept = take(b * mr * 4);
   const size_t o_plist = take(b * mr * 4);
   const size_t o_attn_done = take(b * d.kv_heads * 4);
-  const size_t o_attn_part = take(attn_slots * gq * (d.head_dim + 2) * 4);
+  const size_t o_attn_part = take(attn_slots * gq * (d.head_dim + 4) * 4);
   const size_t o_ent_done = take(b * 4);
   const size_t o_ent_part = take(b * kEntSplit * 3 * 8);
   const size_t o_app = take(b * 4);

@@ -63,7 +63,8 @@ struct Workspace {
 };
 
 constexpr int kEntSplit = 16;
-constexpr int kAttnCtasMax = 148 * 4;
+constexpr int kAttnCtasMax = 160;               // attention CTAs (<= SMs)
+constexpr int kAttnWarpsMax = kAttnCtasMax * 8; // stream-K warps (partial slots)
 
 size_t workspace_layout(const ChessDims& d, void* base, Workspace* ws);
 
@@ -218,6 +219,13 @@ __device__ __forceinline__ double shfl_xor_d(double v, int m) {
   return __shfl_xor_sync(0xffffffffu, v, m);
 }
 
+// Named barrier 1 over the first NT threads: the block helpers below run on a
+// CTA's compute warps while a producer warp (if any) keeps streaming.
+template <int NT>
+__device__ __forceinline__ void block_sync() {
+  asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory");
+}
+
 // ---------------------------------------------------------------------------
 // block-wide helpers (blockDim.x == NT, multiple of 32)
 // ---------------------------------------------------------------------------
@@ -231,7 +239,7 @@ __device__ __forceinline__ int block_exclusive_scan(int v, int* smem_warp, int* 
     if (lane >= o) x += y;
   }
   if (lane == 31) smem_warp[warp] = x;
-  __syncthreads();
+  block_sync<NT>();
   if (warp == 0) {
     int w = (lane < NT / 32) ? smem_warp[lane] : 0;
 #pragma unroll
@@ -241,10 +249,10 @@ __device__ __forceinline__ int block_exclusive_scan(int v, int* smem_warp, int* 
     }
     if (lane < NT / 32) smem_warp[lane] = w;
   }
-  __syncthreads();
+  block_sync<NT>();
   int base = warp > 0 ? smem_warp[warp - 1] : 0;
   *total = smem_warp[NT / 32 - 1];
-  __syncthreads();
+  block_sync<NT>();
   return base + x - v;
 }
 
@@ -258,24 +266,24 @@ __device__ void block_topk_mark(const uint64_t* keys, int n, int k, int* keep, i
                                 int* s_scratch) {
   if (k >= n) {
     for (int i = threadIdx.x; i < n; i += NT) keep[i] = 1;
-    __syncthreads();
+    block_sync<NT>();
     return;
   }
   if (k <= 0) {
     for (int i = threadIdx.x; i < n; i += NT) keep[i] = 0;
-    __syncthreads();
+    block_sync<NT>();
     return;
   }
   uint64_t prefix = 0, mask = 0;
   int kk = k;  // how many still to take among keys matching prefix
   for (int shift = 56; shift >= 0; shift -= 8) {
     for (int b = threadIdx.x; b < 256; b += NT) s_hist[b] = 0;
-    __syncthreads();
+    block_sync<NT>();
     for (int i = threadIdx.x; i < n; i += NT) {
       uint64_t key = keys[i];
       if ((key & mask) == prefix) atomicAdd(&s_hist[(key >> shift) & 255], 1);
     }
-    __syncthreads();
+    block_sync<NT>();
     if (threadIdx.x < 32) {
       // lane l owns bins [255-8l-7, 255-8l] (descending digit order)
       const int lane = threadIdx.x;
@@ -312,12 +320,12 @@ __device__ void block_topk_mark(const uint64_t* keys, int n, int k, int* keep, i
         s_scratch[1] = above;
       }
     }
-    __syncthreads();
+    block_sync<NT>();
     const int digit = s_scratch[0];
     kk -= s_scratch[1];
     prefix |= ((uint64_t)digit) << shift;
     mask |= 0xFFull << shift;
-    __syncthreads();
+    block_sync<NT>();
   }
   // prefix == k-th largest key T; take all keys > T and the first kk keys == T.
   const uint64_t T = prefix;
@@ -331,7 +339,7 @@ __device__ void block_topk_mark(const uint64_t* keys, int n, int k, int* keep, i
     if (i < n) keep[i] = (key > T) || (eq && (taken_eq + pos) < kk);
     taken_eq += tot;
   }
-  __syncthreads();
+  block_sync<NT>();
 }
 
 // Working set of slot s from its sorted semantic list + window + sinks, then
@@ -362,7 +370,7 @@ __device__ void block_build_ws(const ChessState& st, int s, int* s_scratch) {
     s_scratch[0] = a;
     s_scratch[1] = max(a, lo);
   }
-  __syncthreads();
+  block_sync<NT>();
   const int lo = s_scratch[0], hi = s_scratch[1];
   int total = ns + (hi - lo) + (n - c0);
   const int cap = d.max_ws;
@@ -388,7 +396,7 @@ __device__ void block_build_ws(const ChessState& st, int s, int* s_scratch) {
     pv[i] = tag;
   }
   if (threadIdx.x == 0) st.ws_len[s] = min(total, cap);
-  __syncthreads();
+  block_sync<NT>();
 }
 
 // Ordered compaction: out[pos] = idx_of(i) for keep[i] != 0, i ascending.

@@ -99,40 +99,6 @@ __device__ __forceinline__ const double* level_row_ptr<double>(const ChessState&
   return st.page_vec64 + ((int64_t)s * d.max_pages + row) * d.ld;
 }
 
-// 8 elements per thread of a 2048-element slice: element offsets within the
-// slice for vector group v (f32: 2 x float4, f64: 4 x double2).
-template <typename T>
-struct SliceMap;
-template <>
-struct SliceMap<float> {
-  static constexpr int kGroups = 2;
-  static constexpr int kVec = 4;
-  __device__ static int off(int v) { return v * 1024 + (int)threadIdx.x * 4; }
-};
-template <>
-struct SliceMap<double> {
-  static constexpr int kGroups = 4;
-  static constexpr int kVec = 2;
-  __device__ static int off(int v) { return v * 512 + (int)threadIdx.x * 2; }
-};
-
-template <typename T>
-__device__ __forceinline__ void load_group(const T* p, T* out);
-template <>
-__device__ __forceinline__ void load_group<float>(const float* p, float* out) {
-  const float4 v = __ldcs(reinterpret_cast<const float4*>(p));
-  out[0] = v.x;
-  out[1] = v.y;
-  out[2] = v.z;
-  out[3] = v.w;
-}
-template <>
-__device__ __forceinline__ void load_group<double>(const double* p, double* out) {
-  const double2 v = __ldcs(reinterpret_cast<const double2*>(p));
-  out[0] = v.x;
-  out[1] = v.y;
-}
-
 // ---------------------------------------------------------------------------
 // tail: reduce partials, top-k, emit next level (block-wide, one slot)
 // ---------------------------------------------------------------------------
@@ -175,7 +141,7 @@ __device__ void select_tail(const ChessState& st, const Workspace& ws, const Sel
     for (int q = 1; q < ns; ++q) acc = __dadd_rn(acc, __ldcg(part + (int64_t)i * ns + q));
     sc[i] = acc;
   }
-  __syncthreads();
+  block_sync<kNT>();
 
   // level order to run in this tail
   const int lv_begin = level == 3 ? 0 : level;
@@ -204,7 +170,7 @@ __device__ void select_tail(const ChessState& st, const Workspace& ws, const Sel
       }
       keys[i] = score_key(v);
     }
-    __syncthreads();
+    block_sync<kNT>();
     // ceil in double (selection.py:98, 103, 108)
     const int k = (int)ceil(prm.rho[lv] * (double)m);
     block_topk_mark<kNT>(keys, m, k, kept, sm.hist, sm.scratch);
@@ -213,7 +179,7 @@ __device__ void select_tail(const ChessState& st, const Workspace& ws, const Sel
     if (lv < 2) {
       kcount = block_compact<kNT>(kept, m, plist, sm.scratch,
                                   [&](int i) { return cand ? cand[i] : i; });
-      __syncthreads();
+      block_sync<kNT>();
       const int total_children = lv == 0 ? sh.C : sh.P;
       int* out = lv == 0 ? cand1 : cand2;
       expand_children(plist, kcount, fan, total_children, out, &ws.cand_n[4 * s + lv + 1]);
@@ -232,7 +198,7 @@ __device__ void select_tail(const ChessState& st, const Workspace& ws, const Sel
         stats[2] = sh.P;
       }
     }
-    __syncthreads();
+    block_sync<kNT>();
     __threadfence_block();
   }
   if (lv_end == 3) block_build_ws<kNT>(st, s, sm.scratch);
@@ -249,105 +215,212 @@ __device__ void handle_empty_slots(const ChessState& st, const Workspace& ws, co
       ws.cand_n[4 * s + 2] = 0;
       for (int i = 0; i < 8; ++i) st.sel_stats[8 * s + i] = 0;
     }
-    __syncthreads();
+    block_sync<kNT>();
     block_build_ws<kNT>(st, s, sm.scratch);
   }
 }
 
 // ---------------------------------------------------------------------------
 // the scan kernel (one launch per level; level 3 = Alg.1 full scan)
+//
+// Warp 8 is a TMA producer: one cp.async.bulk per (candidate row, 2048-element
+// slice) into a 128 KB shared-memory ring (16 x 8 KB stages for f32 rows).
+// Warps 0-7 consume: each thread owns 8 elements of the slice (conflict-free
+// 16-byte LDS), multiplies by its f64 anchor registers, and the 8 row
+// partials of an item are transpose-reduced across the warp and then across
+// warps in fixed order.  The producer runs ahead across item boundaries and
+// through the per-slot tails, so HBM never idles on the epilogues.
 // ---------------------------------------------------------------------------
+constexpr int kScanCTA = kNT + 32;  // 8 consumer warps + 1 producer warp
+
 template <typename T>
-__global__ void __launch_bounds__(kNT, 1) select_scan_kernel(ChessState st, Workspace ws,
-                                                          SelParams prm, int level) {
-  extern __shared__ int s_prefix[];  // [batch + 1]
-  __shared__ double s_wpart[kScanRows][kWarps];
+struct ScanCfg {
+  static constexpr int kStageBytes = kScanSlice * (int)sizeof(T);
+  static constexpr int kStages = (128 * 1024) / kStageBytes;
+  static constexpr int kVec = 16 / (int)sizeof(T);                // elements per 16-B chunk
+  static constexpr int kGroups = 8 / kVec;                         // chunks per thread
+  __device__ static int off(int v) { return (v * kNT + (int)threadIdx.x) * kVec; }
+};
+
+template <typename T>
+__global__ void __launch_bounds__(kScanCTA, 1) select_scan_kernel(ChessState st, Workspace ws,
+                                                                  SelParams prm, int level) {
+  using SC = ScanCfg<T>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* ring = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
+  uint64_t* full = reinterpret_cast<uint64_t*>(ring + (size_t)SC::kStages * SC::kStageBytes);
+  uint64_t* empty = full + SC::kStages;
+  int* s_prefix = reinterpret_cast<int*>(empty + SC::kStages);  // [batch + 1]
+  __shared__ double s_wpart[2][kScanRows][kWarps];
   __shared__ TailSmem sm;
   __shared__ int s_last;
   const ChessDims& d = st.d;
   const int nb = d.batch;
   const int nsl = ws.n_slices;
-
-  if ((level == 0 || level == 3) && blockIdx.x == 0) handle_empty_slots(st, ws, prm, sm);
-
-  // per-slot item counts -> prefix (block scan in tiles of kNT)
-  int running = 0;
-  for (int b0 = 0; b0 < nb; b0 += kNT) {
-    const int s = b0 + threadIdx.x;
-    int items = 0;
-    if (s < nb) {
-      const int n = level_rows(st, ws, prm, s, level);
-      items = ((n + kScanRows - 1) / kScanRows) * nsl;
-    }
-    int tot;
-    const int pos = block_exclusive_scan<kNT>(items, sm.scratch, &tot);
-    if (s < nb) s_prefix[s] = running + pos;
-    running += tot;
-  }
-  if (threadIdx.x == 0) s_prefix[nb] = running;
-  __syncthreads();
-  const int total = running;
-
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int it = blockIdx.x; it < total; it += gridDim.x) {
-    // slot of this item: last s with s_prefix[s] <= it
+
+  // per-slot item counts -> prefix (warp 0), barrier init (lane 0)
+  if (warp == 0) {
+    int run = 0;
+    for (int b0 = 0; b0 < nb; b0 += 32) {
+      const int s = b0 + lane;
+      int items = 0;
+      if (s < nb) {
+        const int n = level_rows(st, ws, prm, s, level);
+        items = ((n + kScanRows - 1) / kScanRows) * nsl;
+      }
+      int incl = items;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      if (s < nb) s_prefix[s] = run + incl - items;
+      run += __shfl_sync(0xffffffffu, incl, 31);
+    }
+    if (lane == 0) {
+      s_prefix[nb] = run;
+      for (int i = 0; i < SC::kStages; ++i) {
+        mbar_init(&full[i], 1);
+        mbar_init(&empty[i], kWarps);
+      }
+      fence_barrier_init();
+    }
+  }
+  __syncthreads();
+  // contiguous item range per CTA; within a slot items are ordered
+  // (slice, row block) so a CTA reuses one anchor slice across row blocks.
+  const int total = s_prefix[nb];
+  const int it_begin = (int)((int64_t)blockIdx.x * total / gridDim.x);
+  const int it_end = (int)((int64_t)(blockIdx.x + 1) * total / gridDim.x);
+  auto slot_of = [&](int it) {
     int lo = 0, hi = nb;
     while (hi - lo > 1) {
       const int mid = (lo + hi) >> 1;
       if (s_prefix[mid] <= it) lo = mid; else hi = mid;
     }
-    const int s = lo;
+    return lo;
+  };
+  struct ItemPos {
+    int s, n, r0, rows, slice;
+  };
+  auto decode = [&](int it, int s) {
+    ItemPos p;
+    p.s = s;
+    p.n = level_rows(st, ws, prm, s, level);
+    const int nrb = (p.n + kScanRows - 1) / kScanRows;
     const int local = it - s_prefix[s];
-    const int rb = local / nsl, slice = local - rb * nsl;
-    const int n = level_rows(st, ws, prm, s, level);
-    const int r0 = rb * kScanRows;
-    const int64_t ebase = (int64_t)slice * kScanSlice;
-    const LevelShape sh = shape_of(st, s);
+    p.slice = local / nrb;
+    const int rb = local - p.slice * nrb;
+    p.r0 = rb * kScanRows;
+    p.rows = min(kScanRows, p.n - p.r0);
+    return p;
+  };
 
-    // anchor slice (f64) in registers
-    const double* anc = st.anchor + (int64_t)s * d.ld + ebase;
-    double a[8];
-#pragma unroll
-    for (int v = 0; v < SliceMap<T>::kGroups; ++v) {
-      const int o = SliceMap<T>::off(v);
-#pragma unroll
-      for (int e = 0; e < SliceMap<T>::kVec; e += 2) {
-        double2 x = make_double2(0.0, 0.0);
-        if (ebase + o < d.ld) x = *reinterpret_cast<const double2*>(anc + o + e);
-        a[v * SliceMap<T>::kVec + e] = x.x;
-        a[v * SliceMap<T>::kVec + e + 1] = x.y;
-      }
-    }
-    // row loads (a phase's rows issued before use for MLP), f64 accumulation.
-    // f32 rows: 8 rows in flight (64 KB per CTA); f64 rows: 2 phases of 4.
-    constexpr int kPhases = sizeof(T) == 8 ? 2 : 1;
-    constexpr int kRowsPh = kScanRows / kPhases;
-    double acc[kScanRows];
-#pragma unroll
-    for (int phs = 0; phs < kPhases; ++phs) {
-      T vals[kRowsPh][8];
-#pragma unroll
-      for (int rr = 0; rr < kRowsPh; ++rr) {
-        const int r = phs * kRowsPh + rr;
-        const bool row_ok = (r0 + r) < n;
-        const T* rp = row_ok ? level_row_ptr<T>(st, ws, s, level, r0 + r, sh) + ebase : nullptr;
-#pragma unroll
-        for (int v = 0; v < SliceMap<T>::kGroups; ++v) {
-          const int o = SliceMap<T>::off(v);
-          if (row_ok && ebase + o < d.ld) {
-            load_group<T>(rp + o, &vals[rr][v * SliceMap<T>::kVec]);
-          } else {
-#pragma unroll
-            for (int e = 0; e < SliceMap<T>::kVec; ++e) vals[rr][v * SliceMap<T>::kVec + e] = T(0);
-          }
+  if (warp == kWarps) {
+    // ===================== TMA producer =====================
+    if (lane == 0) {
+      int k = 0;
+      int s = -1;
+      LevelShape sh{};
+      for (int it = it_begin; it < it_end; ++it) {
+        if (s < 0 || it >= s_prefix[s + 1]) {
+          s = slot_of(it);
+          sh = shape_of(st, s);
+        }
+        const ItemPos p = decode(it, s);
+        const int64_t ebase = (int64_t)p.slice * kScanSlice;
+        const uint32_t bytes = (uint32_t)(min((int64_t)kScanSlice, d.ld - ebase) * sizeof(T));
+        for (int r = 0; r < p.rows; ++r, ++k) {
+          const int stage = k % SC::kStages;
+          const uint32_t ph = (uint32_t)((k / SC::kStages) & 1);
+          mbar_wait(&empty[stage], ph ^ 1u);
+          mbar_arrive_expect_tx(&full[stage], bytes);
+          tma_load_1d(ring + (size_t)stage * SC::kStageBytes,
+                      level_row_ptr<T>(st, ws, s, level, p.r0 + r, sh) + ebase, bytes, &full[stage]);
         }
       }
+    }
+    return;
+  }
+
+  // ===================== consumers =====================
+  if ((level == 0 || level == 3) && blockIdx.x == 0) handle_empty_slots(st, ws, prm, sm);
+  int k = 0, buf = 0;
+  int s = -1, contributed = 0, a_slice = -1;
+  double a[8];
+  bool in[SC::kGroups];
+  auto flush = [&](int s_done) {
+    // one release per (CTA, slot) run: publishes this CTA's partials
+    block_sync<kNT>();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      const int items_s = s_prefix[s_done + 1] - s_prefix[s_done];
+      const int prev = atomicAdd(&ws.sel_done[s_done], contributed);
+      s_last = (prev + contributed == items_s);
+    }
+    block_sync<kNT>();
+    if (s_last) {
+      __threadfence();
+      select_tail(st, ws, prm, s_done, level, level_rows(st, ws, prm, s_done, level), sm);
+      if (threadIdx.x == 0) ws.sel_done[s_done] = 0;
+      block_sync<kNT>();
+    }
+  };
+  for (int it = it_begin; it < it_end; ++it) {
+    if (s < 0 || it >= s_prefix[s + 1]) {
+      if (s >= 0) flush(s);
+      s = slot_of(it);
+      contributed = 0;
+      a_slice = -1;
+    }
+    const ItemPos p = decode(it, s);
+    const int64_t ebase = (int64_t)p.slice * kScanSlice;
+    if (p.slice != a_slice) {  // anchor slice (f64) in registers; zero beyond ld
+      a_slice = p.slice;
+      const double* anc = st.anchor + (int64_t)s * d.ld + ebase;
 #pragma unroll
-      for (int rr = 0; rr < kRowsPh; ++rr) {
+      for (int v = 0; v < SC::kGroups; ++v) {
+        const int o = SC::off(v);
+        in[v] = ebase + o < d.ld;
+#pragma unroll
+        for (int e = 0; e < SC::kVec; e += 2) {
+          double2 x = make_double2(0.0, 0.0);
+          if (in[v]) x = *reinterpret_cast<const double2*>(anc + o + e);
+          a[v * SC::kVec + e] = x.x;
+          a[v * SC::kVec + e + 1] = x.y;
+        }
+      }
+    }
+    double acc[kScanRows];
+#pragma unroll
+    for (int r = 0; r < kScanRows; ++r) {
+      acc[r] = 0.0;
+      if (r < p.rows) {
+        const int stage = k % SC::kStages;
+        mbar_wait(&full[stage], (uint32_t)((k / SC::kStages) & 1));
+        const T* row = reinterpret_cast<const T*>(ring + (size_t)stage * SC::kStageBytes);
         double x = 0.0;
 #pragma unroll
-        for (int e = 0; e < 8; ++e) x = __fma_rn(a[e], (double)vals[rr][e], x);
-        acc[phs * kRowsPh + rr] = x;
+        for (int v = 0; v < SC::kGroups; ++v) {
+          if (in[v]) {
+            if constexpr (sizeof(T) == 4) {
+              const float4 f = *reinterpret_cast<const float4*>(row + SC::off(v));
+              x = __fma_rn(a[4 * v + 0], (double)f.x, x);
+              x = __fma_rn(a[4 * v + 1], (double)f.y, x);
+              x = __fma_rn(a[4 * v + 2], (double)f.z, x);
+              x = __fma_rn(a[4 * v + 3], (double)f.w, x);
+            } else {
+              const double2 f = *reinterpret_cast<const double2*>(row + SC::off(v));
+              x = __fma_rn(a[2 * v + 0], f.x, x);
+              x = __fma_rn(a[2 * v + 1], f.y, x);
+            }
+          }
+        }
+        acc[r] = x;
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[stage]);
+        ++k;
       }
     }
     // warp transpose-reduce of 8 row partials: 4+2+1 exchanges, then 2 xor adds.
@@ -375,30 +448,19 @@ __global__ void __launch_bounds__(kNT, 1) select_scan_kernel(ChessState st, Work
       acc[0] += shfl_xor_d(acc[0], 2);
       acc[0] += shfl_xor_d(acc[0], 1);
       const int row = ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
-      if ((lane & 3) == 0) s_wpart[row][warp] = acc[0];
+      if ((lane & 3) == 0) s_wpart[buf][row][warp] = acc[0];
     }
-    __syncthreads();
-    if (threadIdx.x < kScanRows && r0 + (int)threadIdx.x < n) {
-      double x = s_wpart[threadIdx.x][0];
+    block_sync<kNT>();  // double-buffered s_wpart: one barrier per item
+    if ((int)threadIdx.x < p.rows) {
+      double x = s_wpart[buf][threadIdx.x][0];
 #pragma unroll
-      for (int w = 1; w < kWarps; ++w) x = __dadd_rn(x, s_wpart[threadIdx.x][w]);
-      ws.part[((int64_t)s * max_rows(d) + r0 + threadIdx.x) * nsl + slice] = x;
+      for (int w = 1; w < kWarps; ++w) x = __dadd_rn(x, s_wpart[buf][threadIdx.x][w]);
+      ws.part[((int64_t)s * max_rows(d) + p.r0 + threadIdx.x) * nsl + p.slice] = x;
     }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      __threadfence();
-      const int items_s = s_prefix[s + 1] - s_prefix[s];
-      const int prev = atomicAdd(&ws.sel_done[s], 1);
-      s_last = (prev == items_s - 1);
-    }
-    __syncthreads();
-    if (s_last) {
-      __threadfence();
-      select_tail(st, ws, prm, s, level, n, sm);
-      if (threadIdx.x == 0) ws.sel_done[s] = 0;
-      __syncthreads();
-    }
+    buf ^= 1;
+    ++contributed;
   }
+  if (s >= 0) flush(s);
 }
 
 // ---------------------------------------------------------------------------
@@ -586,32 +648,31 @@ __global__ void gather_pages_kernel(const int32_t* table, int n_pages, const int
 // ---------------------------------------------------------------------------
 // launch wrappers
 // ---------------------------------------------------------------------------
-int launch_select(const ChessState& st, const Workspace& ws, const SelParams& prm, int grid,
-                  cudaStream_t stream) {
-  const size_t smem = (size_t)(st.d.batch + 1) * sizeof(int);
-  // persistent grid sized by occupancy (the scan keeps 64 KB of loads in
-  // flight per CTA; extra CTAs beyond residency would only serialise)
-  static int occ[2] = {0, 0};
-  const int ti = st.d.summary_dtype == 0 ? 0 : 1;
-  if (occ[ti] == 0) {
-    int o = 0;
-    if (ti == 0)
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, select_scan_kernel<float>, kNT, smem);
-    else
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, select_scan_kernel<double>, kNT, smem);
-    cudaGetLastError();
-    occ[ti] = o > 0 ? o : 1;
+template <typename T>
+static int launch_scan(const ChessState& st, const Workspace& ws, const SelParams& prm, int level,
+                       cudaStream_t stream) {
+  using SC = ScanCfg<T>;
+  const size_t smem = 128 + (size_t)SC::kStages * SC::kStageBytes + 2 * SC::kStages * 8 +
+                      (size_t)(st.d.batch + 1) * sizeof(int);
+  static bool configured = false;
+  if (!configured) {
+    const size_t smem_max = 128 + (size_t)SC::kStages * SC::kStageBytes + 2 * SC::kStages * 8 +
+                            (size_t)(kMaxBatch + 1) * sizeof(int);
+    cudaFuncSetAttribute(select_scan_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_max);
+    configured = true;
   }
-  grid = occ[ti] * num_sms();
-  const int levels[3] = {0, 1, 2};
+  select_scan_kernel<T><<<num_sms(), kScanCTA, smem, stream>>>(st, ws, prm, level);
+  return check_launch("select_scan");
+}
+
+// persistent scan: one CTA per SM (128 KB TMA ring each), one launch per level
+int launch_select(const ChessState& st, const Workspace& ws, const SelParams& prm, int /*grid*/,
+                  cudaStream_t stream) {
   const int nlev = prm.full_scan ? 1 : 3;
   for (int li = 0; li < nlev; ++li) {
-    const int level = prm.full_scan ? 3 : levels[li];
-    if (st.d.summary_dtype == 0)
-      select_scan_kernel<float><<<grid, kNT, smem, stream>>>(st, ws, prm, level);
-    else
-      select_scan_kernel<double><<<grid, kNT, smem, stream>>>(st, ws, prm, level);
-    const int rc = check_launch("select_scan");
+    const int level = prm.full_scan ? 3 : li;
+    const int rc = st.d.summary_dtype == 0 ? launch_scan<float>(st, ws, prm, level, stream)
+                                           : launch_scan<double>(st, ws, prm, level, stream);
     if (rc) return rc;
   }
   return CHESS_OK;
