@@ -1,0 +1,190 @@
+"""Pin the CPU oracle (oracle/pagesel_ref.py) against golden vectors produced
+by the reference itself (tests/golden/make_golden.py).  CPU only.
+
+Bar: bit-exact for every integer/index output and for the f64 arithmetic the
+oracle restates in the reference's operation order (page means, chunk/grid
+sums, anchor, scores), plus the known answers of the reference's own tests
+(test_uncertainty.py:22-31, test_selection.py:149-195, test_hierarchy.py:48-62).
+"""
+
+import json
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from oracle import attention as attn_ref
+from oracle import pagesel_ref as ref
+from paper_2602_20732_b200.config import SelectionConfig
+
+GOLD = Path(__file__).resolve().parent / "golden"
+
+
+def _cfg(arr):
+    B, nc, ng, rg, rc, rp, w, s = arr
+    return SelectionConfig(page_size=int(B), pages_per_chunk=int(nc), chunks_per_grid=int(ng),
+                           rho_grid=float(rg), rho_chunk=float(rc), rho_page=float(rp),
+                           window_pages=int(w), sink_pages=int(s))
+
+
+@pytest.fixture(scope="module")
+def hier():
+    return np.load(GOLD / "hierarchy.npz")
+
+
+@pytest.fixture(scope="module")
+def sel():
+    return np.load(GOLD / "selection.npz")
+
+
+def test_hierarchy_incremental_bitwise(hier):
+    for ci in range(int(hier["n_cases"])):
+        P, B, dim, nc, ng = map(int, hier[f"c{ci}_shape"])
+        h = ref.Hierarchy(dim, nc, ng)
+        keys = hier[f"c{ci}_keys"]
+        for p in range(P):
+            h.fold_page(keys[p], p)
+        assert np.array_equal(h.page_vectors, hier[f"c{ci}_pages"])
+        assert np.array_equal(h.chunk_vectors, hier[f"c{ci}_chunks"])
+        assert np.array_equal(h.grid_vectors, hier[f"c{ci}_grids"])
+        snap = json.loads(str(hier[f"c{ci}_snapshot"]))
+        mine = h.snapshot()
+        for k in ("num_pages", "num_chunks", "num_grids", "checksum_pages", "checksum_chunks",
+                  "checksum_grids"):
+            assert mine[k] == snap[k], (ci, k)
+
+
+def test_hierarchy_bulk_bitwise(hier):
+    for ci in range(int(hier["n_cases"])):
+        P, B, dim, nc, ng = map(int, hier[f"c{ci}_shape"])
+        h = ref.Hierarchy.from_rows(hier[f"c{ci}_pages"], nc, ng)
+        assert np.array_equal(h.chunk_vectors, hier[f"c{ci}_bulk_chunks"])
+        assert np.array_equal(h.grid_vectors, hier[f"c{ci}_bulk_grids"])
+        # incremental == batch within 1e-10 (test_hierarchy.py:79-91)
+        np.testing.assert_allclose(h.grid_vectors, hier[f"c{ci}_grids"], rtol=1e-10, atol=1e-12)
+
+
+def test_hierarchy_order_error():
+    h = ref.Hierarchy(4, 2, 2)
+    h.fold(np.zeros(4), 0)
+    with pytest.raises(ValueError):
+        h.fold(np.zeros(4), 2)
+
+
+def test_selection_instances_bitwise(sel):
+    for i in range(int(sel["n_instances"])):
+        p = f"i{i}_"
+        cfg = _cfg(sel[p + "cfg"])
+        vec = sel[p + "vectors"]
+        tail = sel[p + "tail"]
+        h = ref.Hierarchy.from_rows(vec, cfg.pages_per_chunk, cfg.chunks_per_grid)
+        a, src = ref.anchor(h.page_vectors, cfg.window_pages, tail if len(tail) else None)
+        assert np.array_equal(a, sel[p + "anchor"]), i
+        assert list(src) == list(sel[p + "anchor_sources"])
+        v_all, splits = h.coalesced()
+        assert list(splits) == list(sel[p + "splits"])
+        s = ref.score(v_all, a)
+        assert np.array_equal(s, sel[p + "scores"]), i
+        g, c, _ = splits
+        p2c, c2g = h.parent_maps()
+        got, _ = ref.prune(s[:g], s[g:g + c], s[g + c:], p2c, c2g, cfg.ratios)
+        assert np.array_equal(got, sel[p + "selected"]), i
+        flat = ref.flat_topk(a, h.page_vectors, int(sel[p + "flat_k"]))
+        assert np.array_equal(flat, sel[p + "flat"]), i
+        table = list(sel[p + "table"])
+        pages, prov = ref.working_set(got, len(table), cfg.window_pages, int(sel[p + "sinks"]))
+        assert pages == list(sel[p + "ws_pages"]), i
+        code = {"semantic": 1, "window": 2, "sink": 3}
+        assert [code[prov[q]] for q in pages] == list(sel[p + "ws_prov"])
+        assert ref.gather(table, pages) == list(sel[p + "ws_phys"])
+
+
+def test_known_answer_cascade_and_ties():
+    # test_selection.py:149-161: S_p=[4,3,2,1], rho=(1,1,.5) -> {0,1}
+    p2c, c2g = np.zeros(4, int), np.zeros(1, int)
+    got, _ = ref.prune(np.array([1.0]), np.array([1.0]), np.array([4.0, 3.0, 2.0, 1.0]), p2c, c2g,
+                       (1.0, 1.0, 0.5))
+    assert list(got) == [0, 1]
+    # all-zero tie -> lower indices (test_selection.py:185-195)
+    got, _ = ref.prune(np.zeros(1), np.zeros(1), np.zeros(4), p2c, c2g, (1.0, 1.0, 0.5))
+    assert list(got) == [0, 1]
+    # working-set union example (test_selection.py:242-246)
+    pages, prov = ref.working_set([5], 8, 1, 1)
+    assert pages == [0, 5, 7] and prov == {0: "sink", 5: "semantic", 7: "window"}
+
+
+def test_uncertainty_golden():
+    doc = json.loads((GOLD / "uncertainty.json").read_text())
+    for r in doc["rows"]:
+        assert ref.entropy(r["probs"]) == r["entropy"]
+    k = doc["known"]
+    assert abs(k["uniform8"] - np.log(8)) < 1e-12 and k["onehot"] == 0.0
+    assert abs(k["half_quarter"] - 1.5 * np.log(2)) < 1e-12
+    means, vars_ = [], []
+    for pg in doc["pages"]:
+        m, v, n = ref.page_stats(pg["entropies"])
+        assert (m, v, n) == (pg["mean"], pg["var"], pg["n"])
+        means.append(m)
+        vars_.append(v)
+    cal = doc["calibration"]
+    th = ref.calibrate(means, vars_, cal["percentile"])
+    assert th == (cal["tau_H"], cal["tau_V"])
+    for pg, t in zip(doc["pages"], doc["trigger"]):
+        assert ref.check_trigger(pg["mean"], pg["var"], *th, "joint") == t["joint"]
+        assert ref.check_trigger(pg["mean"], pg["var"], *th, "any") == t["any"]
+    assert ref.check_trigger(th[0], th[1], *th) is False and doc["at_threshold"] is False
+
+
+def test_uncertainty_errors():
+    with pytest.raises(ValueError):
+        ref.entropy([0.5, 0.6])
+    with pytest.raises(ValueError):
+        ref.entropy([-0.1, 1.1])
+    with pytest.raises(ValueError):
+        ref.page_stats([])
+
+
+def _policy(p):
+    if p.startswith("fixed("):
+        return ("fixed", int(p[6:-1]))
+    return (p, None)
+
+
+def test_decode_loop_golden():
+    runs = json.loads((GOLD / "decode_loop.json").read_text())
+    for run in runs:
+        spec = dict(run["spec"])
+        sched = tuple(tuple(x) for x in spec.pop("instability_schedule"))
+        load = ref.workload(**spec, instability_schedule=sched)
+        cfg = _cfg(run["cfg"])
+        tau = run["tau"] if run["policy"] == "dynamic" else None
+        steps, fired = ref.decode_loop(load, cfg, _policy(run["policy"]), tau)
+        assert [s.trigger_fired for s in steps] == run["fired"], run["policy"]
+        assert [s.working_set_size for s in steps] == run["ws_size"]
+        assert [s.recall for s in steps] == run["recall"]
+        assert [s.working_set for s in steps] == [w["pages"] for w in run["working_sets"]]
+
+
+def test_attention_restatement_vs_dense():
+    """The attention oracle is unpinned by the reference (simulate.py:186 only
+    counts ops); check it against an independent dense formulation."""
+    rng = np.random.default_rng(3)
+    n_phys, H, B, d, Hq = 9, 2, 4, 8, 4
+    K = rng.standard_normal((n_phys, H, B, d))
+    V = rng.standard_normal((n_phys, H, B, d))
+    q = rng.standard_normal((2, Hq, d))
+    bt = np.array([[3, 1, 7, 0], [5, 2, 0, 0]])
+    wl, fill = np.array([4, 2]), np.array([3, 1])
+    o, lse = attn_ref.sparse_decode(q, K, V, bt, wl, fill, 0.3)
+    for s in range(2):
+        toks_k, toks_v = [], []
+        for i in range(wl[s]):
+            n = fill[s] if i == wl[s] - 1 else B
+            toks_k.append(K[bt[s, i], :, :n])
+            toks_v.append(V[bt[s, i], :, :n])
+        Ks, Vs = np.concatenate(toks_k, axis=1), np.concatenate(toks_v, axis=1)
+        for h in range(Hq):
+            z = Ks[h // 2] @ q[s, h] * 0.3
+            w = np.exp(z) / np.exp(z).sum()
+            np.testing.assert_allclose(o[s, h], w @ Vs[h // 2], rtol=1e-12, atol=1e-12)
+            np.testing.assert_allclose(lse[s, h], np.log(np.exp(z).sum()), rtol=1e-12)
