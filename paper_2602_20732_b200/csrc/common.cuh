@@ -188,15 +188,35 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
   uint32_t ok;
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
+#ifdef CHESS_MBAR_TEST_WAIT
+      "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+#else
       "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+#endif
       "selp.u32 %0, 1, 0, p;\n\t}"
       : "=r"(ok)
       : "r"(smem_u32(bar)), "r"(parity)
       : "memory");
   return ok != 0;
 }
+// Bounded wait: a pipeline that never completes (lost TMA transaction,
+// protocol bug) traps after ~4 s of wall time instead of hanging the device;
+// the trap surfaces as a CUDA error at the next synchronisation.
+__device__ __forceinline__ uint64_t global_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  if (mbar_try_wait(bar, parity)) return;
+  const uint64_t t0 = global_ns();
+  uint32_t polls = 0;
   while (!mbar_try_wait(bar, parity)) {
+    if ((++polls & 1023u) == 0 && global_ns() - t0 > 4000000000ull) {
+      printf("chess: mbarrier wait timed out (block %d thread %d parity %u)\n", blockIdx.x,
+             threadIdx.x, parity);
+      asm volatile("trap;");
+    }
   }
 }
 // 1-D bulk global->shared copy completing on an mbarrier (SASS: UBLKCP).
@@ -208,6 +228,12 @@ __device__ __forceinline__ void tma_load_1d(void* dst_smem, const void* src_gmem
       "l"(src_gmem), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
+
+// GPU-scope acquire/release fence: orders this thread's prior global writes
+// before (and later reads after) a flag/counter handshake between CTAs.  Far
+// cheaper than __threadfence() (fence.sc.gpu + L1 invalidate, SASS ERRBAR +
+// CCTL.IVALL), which showed up as microseconds per split-K merge.
+__device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
 
 // Programmatic dependent launch controls (griddepcontrol, sm_90+).
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }

@@ -3,24 +3,28 @@
 // Not present in the reference: pagesel only counts attention work
 // (simulate.py:186, B*2*|WS|*B*D).  The paper runs FlashInfer's paged decode
 // over the reconstructed context; oracle restated in
-// oracle/attention.py (fp64 softmax(q K^T / sqrt(d)) V over the working set
-// in increasing logical order; rows >= fill never contribute).
+// oracle/attention.py (fp64 softmax(q K^T * scale) V over the working set in
+// increasing logical order; rows >= fill never contribute).
 //
-// B200 design:
-//  * unit of work = 16 tokens of one (slot, kv head, page); the units of a
-//    layer are cut into equal contiguous ranges, one per WARP (stream-K over
-//    8 warps x 148 SMs), so every warp streams the same bytes (+-1 unit);
-//  * every warp is its own producer: lane 0 issues 2-D TMA tensor loads
-//    (cp.async.bulk.tensor, 128B swizzle, 8-row boxes) of the unit's K and V
-//    into a private 3-stage shared-memory ring guarded by mbarriers — no
-//    CTA-wide barrier anywhere in the main loop;
-//  * QK^T and PV run on the tensor cores with mma.sync m16n8k16 (bf16 in,
-//    fp32 accumulate): the GQA group's q heads fill the M=16 rows, tokens are
-//    N (QK) / K (PV); ldmatrix reads the swizzled tiles conflict-free and the
-//    S accumulator fragments are reused in registers as the P operand;
-//  * segments split across warps are merged by the last warp to finish
-//    (atomic counter), in warp order — deterministic.
+// B200 design — HBM-bound, one persistent CTA per SM:
+//  * work list = every (slot, kv head, working-set page) of the layer, laid
+//    out segment by segment (segment = one (slot, kv head)); CTA c owns the
+//    contiguous page range [c*N/G, (c+1)*N/G) (stream-K at page granularity,
+//    so every CTA streams the same bytes +-1 page);
+//  * warp 8 is the TMA producer: it reads the block-table entries of 32
+//    upcoming pages with one coalesced load (prefetched one batch ahead), then
+//    lane 0 issues 2-D tensor loads (128B swizzle, [64 cols x B rows] boxes)
+//    of each page's K and V into an S-stage shared-memory ring — no dependent
+//    global load sits between two TMA issues;
+//  * warps 0-7 consume pages round-robin (page j -> warp j % 8): QK^T and PV
+//    on the tensor cores with mma.sync m16n8k16 (bf16 in, fp32 accumulate;
+//    the GQA group's q heads are the M rows), online softmax in registers;
+//  * at the end of each segment piece the 8 warp states are merged in smem in
+//    warp order; a segment split across CTAs is merged by the last CTA to
+//    finish it (atomic counter), in CTA order — deterministic.
 #include <cudaTypedefs.h>
+
+#include <cstdlib>
 
 #include "common.cuh"
 
@@ -28,10 +32,12 @@ namespace chess {
 
 namespace {
 
-constexpr int kWarpsPerCta = 8;
-constexpr int kThreads = kWarpsPerCta * 32;
+constexpr int kConsumers = 8;
+constexpr int kMinPiece = 4;  // piece mode: pages per piece >= 4 (bounds the merge fan-in)
+constexpr int kThreads = (kConsumers + 1) * 32;
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kLn2 = 0.6931471805599453f;
+constexpr int kSmemBudget = 227 * 1024 - 256;  // minus static smem
 
 struct AttnArgs {
   const __nv_bfloat16* q;
@@ -41,29 +47,49 @@ struct AttnArgs {
   float* lse;
   float scale_log2;  // softmax_scale * log2(e)
   int layer;
+  int mode;  // debug (CHESS_ATTN_MODE): 0 normal, 1 loads only (no math), 2 math only (no K/V loads), 5 exit at entry, 6 exit after the prologue
 };
+
+// Debug timeline (read by chess_debug_attn_trace): per CTA globaltimer stamps
+// {entry, prologue done, first page ready, consumers done, exit}, kept for
+// the last launch of each layer parity.
+__device__ unsigned long long g_attn_trace[2][256][8];
+__device__ __forceinline__ void trace(int which, int layer) {
+  if (threadIdx.x == 0 && blockIdx.x < 256) g_attn_trace[layer & 1][blockIdx.x][which] = global_ns();
+}
 
 template <int HD, int GQ, int B>
 struct Cfg {
-  static constexpr int kUT = 16;                     // tokens per unit
-  static constexpr int kUPP = B / kUT;               // units per page
-  static constexpr int kHalves = HD / 64;            // 128-byte column boxes
-  static constexpr int kUnitBytes = kUT * HD * 2;    // K (or V) bytes of a unit
-  static constexpr int kStageBytes = 2 * kUnitBytes;
-  static constexpr int kStages = HD == 128 ? 3 : 6;  // per warp
-  static constexpr int kNT = HD / 8;                 // PV n-tiles
-  static constexpr int kKS = HD / 16;                // QK k-steps
-  static constexpr size_t kSmem = (size_t)kWarpsPerCta * kStages * kStageBytes + 1024 /*align*/ +
-                                  kWarpsPerCta * kStages * 8 + (kMaxBatch + 1) * 4;
+  static constexpr int kCB = HD / 64;                  // 128-byte column blocks
+  static constexpr int kPageBytes = B * HD * 2;        // K (or V) bytes of a page
+  static constexpr int kStageBytes = 2 * kPageBytes;
+  static constexpr int kRow = HD + 4;                  // state row: o[HD], m, l, pad
+  static constexpr int kStateBytes = kConsumers * GQ * kRow * 4;
+  static constexpr int kQBytes = GQ * HD * 2;          // one GQA group's q rows (bf16)
+  static constexpr int kQSlots = 2;
+  static constexpr int kTables = (kMaxBatch + 1) * 4 * 4;
+  static constexpr int kMisc = kTables + 64 * 8 + 64 + 1024;  // tables, barriers, counters, align
+  static constexpr int kStagesRaw = (kSmemBudget - kStateBytes - kQSlots * kQBytes - kMisc) / kStageBytes;
+  static constexpr int kStages = kStagesRaw > 32 ? 32 : kStagesRaw;
+  static constexpr int kMT = B / 16;                   // QK m-tiles (16 tokens each)
+  static constexpr int kKS = HD / 16;                  // QK k-steps over d
+  static constexpr int kDT = HD / 16;                  // PV m-tiles (16 d each)
+  static constexpr int kPK = B / 16;                   // PV k-steps (16 tokens each)
+  static constexpr int kEPL = GQ * HD / 32;            // merge: state elements per lane
+  static constexpr size_t kSmem = 1024 + (size_t)kStages * kStageBytes + kStateBytes +
+                                  kQSlots * kQBytes + (2 * kStages + 2 * kQSlots) * 8 + 64 + kTables;
+  static_assert(kStages >= 4, "ring too shallow");
+  static_assert(GQ <= 8, "one GQA group per n8 tile");
+  static_assert(kEPL >= 2 && kEPL % 2 == 0 && HD % kEPL == 0, "merge lane mapping");
 };
 
-__device__ __forceinline__ void mma_bf16(float (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2,
-                                         uint32_t a3, uint32_t b0, uint32_t b1) {
+__device__ __forceinline__ void mma_bf16(float (&c)[4], const uint32_t (&a)[4], uint32_t b0,
+                                         uint32_t b1) {
   asm volatile(
       "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
       "{%8,%9}, {%0,%1,%2,%3};"
       : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
-      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
 
 __device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t (&r)[4]) {
@@ -76,6 +102,12 @@ __device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t (&r)[4]) {
                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
                : "r"(addr));
 }
+// 8x8 b16 register transpose across the warp
+__device__ __forceinline__ uint32_t movm_t(uint32_t x) {
+  uint32_t y;
+  asm volatile("movmatrix.sync.aligned.m8n8.trans.b16 %0, %1;" : "=r"(y) : "r"(x));
+  return y;
+}
 
 __device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map, int c0, int c1,
                                             int c2, uint32_t bar) {
@@ -86,22 +118,55 @@ __device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map
       : "memory");
 }
 
+__device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
+}
+
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
   return *reinterpret_cast<uint32_t*>(&v);
 }
 
-// swizzled (128B) address of 16-byte chunk `chunk` (0..HD/8-1) of tile row `row`
+// 128B-swizzled address of 16-byte chunk `chunk` (0..HD/8-1) of page row `row`
+// inside one K or V page tile laid out as [HD/64 column blocks][B rows][128 B].
+template <int B>
 __device__ __forceinline__ uint32_t swz(uint32_t base, int row, int chunk) {
-  return base + (uint32_t)((chunk >> 3) * (16 * 128) + row * 128 + (((chunk & 7) ^ (row & 7)) << 4));
+  return base + (uint32_t)((chunk >> 3) * (B * 128) + row * 128 + (((chunk & 7) ^ (row & 7)) << 4));
 }
 
-struct Unit {
-  int s, h, j;   // slot, kv head, unit index within the segment
-  int ups;       // units in this segment
-  int64_t seg_begin;
-};
+// named barrier 2 over the consumer warps only
+__device__ __forceinline__ void consumer_sync() {
+  asm volatile("bar.sync 2, %0;" ::"n"(kConsumers * 32) : "memory");
+}
 
+__device__ __forceinline__ int ld_acquire_cta(const int* p) {
+  int v;
+  asm volatile("ld.acquire.cta.shared::cta.b32 %0, [%1];" : "=r"(v) : "r"(smem_u32(p)) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_cta(int* p, int v) {
+  asm volatile("st.release.cta.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(p)), "r"(v) : "memory");
+}
+
+// Consumer math layout ("tokens as M"): per page, S^T = K q^T with the
+// page's tokens as the MMA M dimension (16 per tile), the GQA group's q heads
+// as N (8, padded) and d as K; then O^T += V^T P^T with d as M, heads as N
+// and tokens as K.  The S^T accumulator of an 8-token block is exactly the
+// P^T B-fragment after one movmatrix transpose, so P never touches smem.
+// Per 32-token page: 2x8 + 8x2 = 32 HMMA (half of the heads-as-M layout).
+//
+// Synchronisation: consumers block only on data.
+//  * K/V ring: full/empty mbarriers per stage.  A stage is shared by
+//    different consumer warps, so before waiting on page j's full barrier a
+//    consumer checks the producer's `issued` counter (> j): page j issued
+//    implies page j-S was consumed, so the parity test cannot alias an older
+//    phase of the stage.
+//  * q ring (2 slots): the producer bulk-copies each piece's GQA q rows next
+//    to the piece's first page; consumers release a slot after reading it.
+//  * piece states: each consumer warp drops its (m, l, o) into a state slot
+//    and moves on; the last warp to arrive (smem atomic) merges the 8 states
+//    in warp order and writes the output, or the split-segment partial and the
+//    cross-CTA combine.  The slot is reopened via `st_next`.
 template <int HD, int GQ, int B>
 __global__ void __launch_bounds__(kThreads, 1)
     sparse_decode_kernel(ChessState st, Workspace ws, AttnArgs args,
@@ -110,25 +175,49 @@ __global__ void __launch_bounds__(kThreads, 1)
   using C = Cfg<HD, GQ, B>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* stages = smem;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(stages + (size_t)kWarpsPerCta * C::kStages * C::kStageBytes);
-  int* prefix = reinterpret_cast<int*>(bars + kWarpsPerCta * C::kStages);
+  uint8_t* ring = smem;
+  float* stv = reinterpret_cast<float*>(ring + (size_t)C::kStages * C::kStageBytes);
+  uint8_t* qbuf = reinterpret_cast<uint8_t*>(stv + kConsumers * GQ * C::kRow);
+  uint64_t* full = reinterpret_cast<uint64_t*>(qbuf + C::kQSlots * C::kQBytes);
+  uint64_t* empty = full + C::kStages;
+  uint64_t* qfull = empty + C::kStages;
+  uint64_t* qempty = qfull + C::kQSlots;
+  int* ctr = reinterpret_cast<int*>(qempty + C::kQSlots);  // [0] issued, [1] st_cnt, [2] st_next
+  int* prefix = ctr + 16;                                   // [nb + 1] pages before slot s
+  int* s_np = prefix + kMaxBatch + 1;                       // [nb] pages per segment of slot s
+  int* s_fill = s_np + kMaxBatch;                            // [nb] valid rows of the last page
+  int* ppre = s_fill + kMaxBatch;                            // [nb + 1] pieces before slot s (piece mode)
   const ChessDims& d = st.d;
   const int H = d.kv_heads;
   const int nb = d.batch;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
-  pdl_wait();
-  // units per slot: H * ((ws_len-1)*UPP + ceil(fill/16)); prefix over slots
+  if (threadIdx.x == kConsumers * 32) {
+    prefetch_tmap(&kmap);
+    prefetch_tmap(&vmap);
+  }
+  trace(0, args.layer);
+  if (threadIdx.x == 0 && blockIdx.x < 256) g_attn_trace[args.layer & 1][blockIdx.x][4] = 0;
+  if (args.mode == 5) return;  // debug: launch overhead only
+  // Everything up to the q load reads state that was final before the
+  // previous kernel started (KV pool, block table, ws_len, fill), so the
+  // prologue, the block-table fetch and the first K/V TMA loads overlap the
+  // previous kernel's tail under PDL; griddepcontrol.wait guards the q reads
+  // and every write (out, lse, split partials, counters).
+  // pages per segment: np = ws_len - 1 + (fill > 0); prefix over slots (x H)
   if (warp == 0) {
     int run = 0;
     for (int b0 = 0; b0 < nb; b0 += 32) {
       const int s = b0 + lane;
-      int x = 0;
+      int np = 0, fill = 0;
       if (s < nb) {
         const int wl = st.ws_len[s];
-        if (wl > 0) x = H * ((wl - 1) * C::kUPP + (st.tail_fill[s] + C::kUT - 1) / C::kUT);
+        fill = min(st.tail_fill[s], B);
+        if (wl > 0) np = wl - 1 + (fill > 0 ? 1 : 0);
+        s_np[s] = np;
+        s_fill[s] = fill > 0 ? fill : B;
       }
+      const int x = np * H;
       int incl = x;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
@@ -139,303 +228,455 @@ __global__ void __launch_bounds__(kThreads, 1)
       run += __shfl_sync(0xffffffffu, incl, 31);
     }
     if (lane == 0) prefix[nb] = run;
-  }
-  __syncthreads();
-  pdl_launch_dependents();
-
-  const int64_t N = prefix[nb];
-  const int64_t NW = min((int64_t)gridDim.x * kWarpsPerCta, N);
-  const int64_t gw = (int64_t)blockIdx.x * kWarpsPerCta + warp;
-  if (gw >= NW) return;
-  const int64_t u_begin = gw * N / NW, u_end = (gw + 1) * N / NW;
-  const int n_units = (int)(u_end - u_begin);
-
-  uint8_t* my_stages = stages + (size_t)warp * C::kStages * C::kStageBytes;
-  uint64_t* my_bars = bars + warp * C::kStages;
-  if (lane == 0) {
-    for (int i = 0; i < C::kStages; ++i) mbar_init(&my_bars[i], 1);
+    // piece mode (segments <= CTAs): every segment of np pages is split into
+    // k_s = min(k, np) near-equal pieces, k = floor(G / segments), one piece
+    // per CTA; piece prefix over slots.
+    const int G0 = min((int)gridDim.x, run);
+    int nseg = 0;
+    for (int b0 = 0; b0 < nb; b0 += 32) {
+      const int s = b0 + lane;
+      nseg += __popc(__ballot_sync(0xffffffffu, s < nb && s_np[s] > 0)) * H;
+    }
+    const int kp = nseg > 0 && nseg <= G0 ? G0 / nseg : 0;  // 0: stream-K mode
+    int prun = 0;
+    for (int b0 = 0; b0 < nb; b0 += 32) {
+      const int s = b0 + lane;
+      const int x = (s < nb) ? min(kp, (s_np[s] + kMinPiece - 1) / kMinPiece) * H : 0;
+      int incl = x;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      if (s < nb) ppre[s] = prun + incl - x;
+      prun += __shfl_sync(0xffffffffu, incl, 31);
+    }
+    if (lane == 0) {
+      ppre[nb] = prun;
+      ctr[3] = kp;
+    }
+  } else if (warp == kConsumers && lane == 0) {
+    for (int i = 0; i < C::kStages; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < C::kQSlots; ++i) {
+      mbar_init(&qfull[i], 1);
+      mbar_init(&qempty[i], kConsumers);
+    }
+    ctr[0] = 0;
+    ctr[1] = 0;
+    ctr[2] = 0;
     fence_barrier_init();
   }
-  __syncwarp();
+  __syncthreads();
+  trace(1, args.layer);
+  pdl_launch_dependents();
 
-  // ---- unit walker ----
-  auto locate = [&](int64_t u) {
+  if (args.mode == 6) return;  // debug: launch + prologue
+  const int N = prefix[nb];
+  const int kp = ctr[3];
+  // stream-K: CTA c owns pages [c*N/G, (c+1)*N/G), G = min(grid, N).
+  // piece mode: CTA c owns piece c of the segment-aligned split.
+  const int G = kp > 0 ? ppre[nb] : min((int)gridDim.x, N);
+  const int c = blockIdx.x;
+  if (c >= G) return;
+  int u_begin, u_end;
+  if (kp > 0) {
+    int lo = 0, hi = nb;
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (ppre[mid] <= c) lo = mid; else hi = mid;
+    }
+    const int np = s_np[lo], ks = min(kp, (np + kMinPiece - 1) / kMinPiece);
+    const int r = c - ppre[lo], h = r / ks, idx = r - h * ks;
+    const int base = prefix[lo] + h * np;
+    u_begin = base + (int)((int64_t)idx * np / ks);
+    u_end = base + (int)((int64_t)(idx + 1) * np / ks);
+  } else {
+    u_begin = (int)((int64_t)c * N / G);
+    u_end = (int)((int64_t)(c + 1) * N / G);
+  }
+
+  // global page index u -> (slot, head, page within segment)
+  auto locate = [&](int u, int& s, int& h, int& p) {
     int lo = 0, hi = nb;
     while (hi - lo > 1) {
       const int mid = (lo + hi) >> 1;
       if (prefix[mid] <= u) lo = mid; else hi = mid;
     }
-    Unit x;
-    x.s = lo;
-    const int wl = st.ws_len[lo];
-    x.ups = (wl - 1) * C::kUPP + (st.tail_fill[lo] + C::kUT - 1) / C::kUT;
-    const int64_t r = u - prefix[lo];
-    x.h = (int)(r / x.ups);
-    x.j = (int)(r - (int64_t)x.h * x.ups);
-    x.seg_begin = prefix[lo] + (int64_t)x.h * x.ups;
-    return x;
-  };
-  auto advance = [&](Unit& x) {
-    if (++x.j >= x.ups) {
-      x.seg_begin += x.ups;
-      x.j = 0;
-      if (++x.h >= H) {
-        x.h = 0;
-        do {
-          ++x.s;
-        } while (x.s < nb && st.ws_len[x.s] == 0);
-        if (x.s < nb)
-          x.ups = (st.ws_len[x.s] - 1) * C::kUPP + (st.tail_fill[x.s] + C::kUT - 1) / C::kUT;
-      }
-    }
-  };
-  auto unit_rows = [&](const Unit& x) {
-    const int page = x.j / C::kUPP;
-    const int half = x.j - page * C::kUPP;
-    const int wl = st.ws_len[x.s];
-    const int fill = (page == wl - 1) ? st.tail_fill[x.s] : B;
-    return min(C::kUT, fill - half * C::kUT);
+    s = lo;
+    const int r = u - prefix[lo];
+    h = r / s_np[lo];
+    p = r - h * s_np[lo];
   };
 
-  // ---- producer (lane 0): TMA loads of unit x into stage ----
-  auto issue = [&](const Unit& x, int stage) {
-    const int page = x.j / C::kUPP;
-    const int half = x.j - page * C::kUPP;
-    const int valid = unit_rows(x);
-    const int nrb = valid > 8 ? 2 : 1;
-    const int64_t phys = st.block_table[(int64_t)x.s * d.max_ws + page];
-    const int row0 = (int)((phys * H + x.h) * B + half * C::kUT);
-    const uint32_t bar = smem_u32(&my_bars[stage]);
-    const uint32_t kdst = smem_u32(my_stages + (size_t)stage * C::kStageBytes);
-    const uint32_t vdst = kdst + C::kUnitBytes;
-    mbar_arrive_expect_tx(&my_bars[stage], (uint32_t)(2 * C::kHalves * nrb * 1024));
+  if (warp == kConsumers) {
+    // ===================== TMA producer =====================
+    const int n = u_end - u_begin;
+    // lane -> page base+lane: first pool row of (page, head); piece-start tag
+    auto fetch = [&](int base, int& row0, int& tag) {
+      row0 = 0;
+      tag = -1;
+      if (base + lane < n) {
+        int s, h, p;
+        locate(u_begin + base + lane, s, h, p);
+        const int pid = __ldg(st.block_table + (int64_t)s * d.max_ws + p);
+        row0 = (pid * H + h) * B;
+        if (p == 0 || base + lane == 0) tag = s * 256 + h;
+      }
+    };
+    int cur_row, cur_tag, nxt_row = 0, nxt_tag = -1;
+    fetch(0, cur_row, cur_tag);
+    int stage = 0, qk = 0;
+    uint32_t ph = 0;
+    for (int base = 0; base < n; base += 32) {
+      if (base + 32 < n) fetch(base + 32, nxt_row, nxt_tag);
+      const int cnt = min(32, n - base);
+      for (int i = 0; i < cnt; ++i) {
+        const int row0 = __shfl_sync(0xffffffffu, cur_row, i);
+        const int tag = __shfl_sync(0xffffffffu, cur_tag, i);
+        if (lane == 0) {
+          if (tag >= 0) {  // first page of a piece: its q rows into the q ring
+            if (qk == 0) pdl_wait();
+            const int qs = qk & 1;
+            mbar_wait(&qempty[qs], (uint32_t)(((qk >> 1) & 1) ^ 1));
+            mbar_arrive_expect_tx(&qfull[qs], (uint32_t)C::kQBytes);
+            const __nv_bfloat16* qsrc = args.q + (int64_t)(tag >> 8) * args.q_stride + (int64_t)(tag & 255) * GQ * HD;
+            tma_load_1d(qbuf + qs * C::kQBytes, qsrc, (uint32_t)C::kQBytes, &qfull[qs]);
+            ++qk;
+          }
+          mbar_wait(&empty[stage], ph ^ 1u);
+          if (args.mode == 2) {
+            mbar_arrive(&full[stage]);
+          } else {
+            mbar_arrive_expect_tx(&full[stage], (uint32_t)C::kStageBytes);
+            const uint32_t kdst = smem_u32(ring + (size_t)stage * C::kStageBytes);
+            const uint32_t bar = smem_u32(&full[stage]);
 #pragma unroll
-    for (int hb = 0; hb < C::kHalves; ++hb) {
-      for (int rb = 0; rb < nrb; ++rb) {
-        const uint32_t off = hb * (C::kUT * 128) + rb * 1024;
-        tma_load_3d(kdst + off, &kmap, hb * 64, row0 + rb * 8, args.layer, bar);
-        tma_load_3d(vdst + off, &vmap, hb * 64, row0 + rb * 8, args.layer, bar);
+            for (int cb = 0; cb < C::kCB; ++cb) {
+              tma_load_3d(kdst + cb * (B * 128), &kmap, cb * 64, row0, args.layer, bar);
+              tma_load_3d(kdst + C::kPageBytes + cb * (B * 128), &vmap, cb * 64, row0, args.layer, bar);
+            }
+          }
+          st_release_cta(&ctr[0], base + i + 1);
+        }
+        if (++stage == C::kStages) {
+          stage = 0;
+          ph ^= 1u;
+        }
       }
+      cur_row = nxt_row;
+      cur_tag = nxt_tag;
     }
-  };
-
-  Unit cu = locate(u_begin);
-  {
-    Unit pu = cu;
-    if (lane == 0) {
-      for (int k = 0; k < C::kStages && k < n_units; ++k) {
-        issue(pu, k);
-        advance(pu);
-      }
-    }
+    return;
   }
-  Unit pu = cu;  // producer cursor (lane 0 only meaningful), kStages ahead
-  for (int k = 0; k < C::kStages && k < n_units; ++k) advance(pu);
 
-  // ---- consumer state ----
+  // ===================== consumers =====================
   const int g = lane >> 2, t = lane & 3;
-  uint32_t qa[C::kKS][2];
-  float o[C::kNT][4];
-  float m_run, l_run;
-  auto load_q = [&](const Unit& x) {
-    const __nv_bfloat16* qp = args.q + (int64_t)x.s * args.q_stride + ((int64_t)x.h * GQ + g) * HD;
-#pragma unroll
-    for (int kk = 0; kk < C::kKS; ++kk) {
-      if (g < GQ) {
-        qa[kk][0] = *reinterpret_cast<const uint32_t*>(qp + kk * 16 + 2 * t);
-        qa[kk][1] = *reinterpret_cast<const uint32_t*>(qp + kk * 16 + 8 + 2 * t);
-      } else {
-        qa[kk][0] = qa[kk][1] = 0u;
-      }
-    }
-#pragma unroll
-    for (int nt = 0; nt < C::kNT; ++nt) o[nt][0] = o[nt][1] = o[nt][2] = o[nt][3] = 0.f;
-    m_run = -INFINITY;
-    l_run = 0.f;
-  };
-  load_q(cu);
+  const int lr = lane & 7, lm = lane >> 3;  // ldmatrix: row in matrix, matrix index
+  int u = u_begin, k = 0;
+  while (u < u_end) {
+    int s, h, p0;
+    locate(u, s, h, p0);
+    const int np = s_np[s];
+    const int seg_begin = prefix[s] + h * np;
+    const int seg_end = seg_begin + np;
+    const int piece_end = min(seg_end, u_end);
+    const int piece_n = piece_end - u;
+    const int j0 = u - u_begin;  // CTA-local index of the piece's first page
+    const int last_fill = s_fill[s];
 
-  const int mr = lane & 7, mm = lane >> 3;  // ldmatrix row / matrix of this lane
-  for (int k = 0; k < n_units; ++k) {
-    const int stage = k % C::kStages;
-    const uint32_t parity = (uint32_t)((k / C::kStages) & 1);
-    const int valid = unit_rows(cu);
-    mbar_wait(&my_bars[stage], parity);
-    uint8_t* kst_p = my_stages + (size_t)stage * C::kStageBytes;
-    const uint32_t kst = smem_u32(kst_p);
-    const uint32_t vst = kst + C::kUnitBytes;
-    if (valid < C::kUT) {
-      // rows >= valid hold stale / never-written data: zero V so P*V stays finite
-      for (int idx = lane; idx < (C::kUT - valid) * C::kHalves * 8; idx += 32) {
-        const int r = valid + idx / (C::kHalves * 8);
-        const int ch = idx % (C::kHalves * 8);
-        *reinterpret_cast<uint4*>(kst_p + C::kUnitBytes + (swz(0, r, ch))) = make_uint4(0, 0, 0, 0);
+    // q^T B-fragments from the q ring: b[ks][0] = q[g][16ks+2t..], b[ks][1] = q[g][16ks+8+2t..]
+    uint32_t qb[C::kKS][2];
+    {
+      const int qs = k & 1;
+      mbar_wait(&qfull[qs], (uint32_t)((k >> 1) & 1));
+      const uint8_t* qrow = qbuf + qs * C::kQBytes + g * HD * 2;
+#pragma unroll
+      for (int ks = 0; ks < C::kKS; ++ks) {
+        if (g < GQ) {
+          qb[ks][0] = *reinterpret_cast<const uint32_t*>(qrow + (ks * 16 + 2 * t) * 2);
+          qb[ks][1] = *reinterpret_cast<const uint32_t*>(qrow + (ks * 16 + 8 + 2 * t) * 2);
+        } else {
+          qb[ks][0] = qb[ks][1] = 0u;
+        }
       }
       __syncwarp();
+      if (lane == 0) mbar_arrive(&qempty[qs]);
     }
+    // O^T accumulators: o[dt] = rows d 16dt+g (+8), cols heads 2t, 2t+1
+    float o[C::kDT][4];
+#pragma unroll
+    for (int dt = 0; dt < C::kDT; ++dt) o[dt][0] = o[dt][1] = o[dt][2] = o[dt][3] = 0.f;
+    float m_run[2] = {-INFINITY, -INFINITY}, l_run[2] = {0.f, 0.f};  // heads 2t, 2t+1
 
-    // ---- S = Q K^T (16 q rows x 16 tokens) ----
-    float sacc[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
-#pragma unroll
-    for (int kp = 0; kp < C::kKS / 2; ++kp) {
-#pragma unroll
-      for (int j = 0; j < 2; ++j) {
-        uint32_t b[4];
-        ldsm_x4(swz(kst, 8 * j + mr, 4 * kp + mm), b);
-        mma_bf16(sacc[j], qa[2 * kp][0], 0u, qa[2 * kp][1], 0u, b[0], b[1]);
-        mma_bf16(sacc[j], qa[2 * kp + 1][0], 0u, qa[2 * kp + 1][1], 0u, b[2], b[3]);
+    for (int i = warp; i < piece_n; i += kConsumers) {
+      const int j = j0 + i;
+      const int valid = (p0 + i == np - 1) ? last_fill : B;
+      const int stage = j % C::kStages;
+      const uint32_t phase = (uint32_t)((j / C::kStages) & 1);
+      if (lane == 0) {
+        while (ld_acquire_cta(&ctr[0]) <= j) {
+        }
       }
-    }
-    // ---- online softmax over this unit's tokens (row g) ----
-    float sv[4];
+      __syncwarp();
+      mbar_wait(&full[stage], phase);
+      if (j == 0 && warp == 0) trace(2, args.layer);
+      const uint32_t kst = smem_u32(ring + (size_t)stage * C::kStageBytes);
+      const uint32_t vst = kst + C::kPageBytes;
+      if (args.mode != 1) {
+        // ---- S^T = K q^T : tokens (M) x heads (N) ----
+        float sc[C::kMT][4];
 #pragma unroll
-    for (int j = 0; j < 2; ++j) {
+        for (int mt = 0; mt < C::kMT; ++mt) sc[mt][0] = sc[mt][1] = sc[mt][2] = sc[mt][3] = 0.f;
 #pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int tok = 8 * j + 2 * t + e;
-        const float x = sacc[j][e] * args.scale_log2;
-        sv[2 * j + e] = (tok < valid && x == x) ? x : -INFINITY;
+        for (int ks = 0; ks < C::kKS; ++ks) {
+#pragma unroll
+          for (int mt = 0; mt < C::kMT; ++mt) {
+            uint32_t a[4];
+            ldsm_x4(swz<B>(kst, 16 * mt + lr + 8 * (lm & 1), 2 * ks + (lm >> 1)), a);
+            mma_bf16(sc[mt], a, qb[ks][0], qb[ks][1]);
+          }
+        }
+        // ---- online softmax per head (2t, 2t+1) over tokens 16mt + g (+8) ----
+        float mx[2] = {-INFINITY, -INFINITY};
+#pragma unroll
+        for (int mt = 0; mt < C::kMT; ++mt) {
+#pragma unroll
+          for (int r = 0; r < 4; ++r) {
+            const int tok = 16 * mt + g + 8 * (r >> 1);
+            const float x = sc[mt][r] * args.scale_log2;
+            sc[mt][r] = (tok < valid && x == x) ? x : -INFINITY;
+            mx[r & 1] = fmaxf(mx[r & 1], sc[mt][r]);
+          }
+        }
+        float alpha[2];
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          mx[e] = fmaxf(mx[e], __shfl_xor_sync(0xffffffffu, mx[e], 4));
+          mx[e] = fmaxf(mx[e], __shfl_xor_sync(0xffffffffu, mx[e], 8));
+          mx[e] = fmaxf(mx[e], __shfl_xor_sync(0xffffffffu, mx[e], 16));
+          const float m_new = fmaxf(m_run[e], mx[e]);
+          alpha[e] = exp2f(m_run[e] - m_new);
+          m_run[e] = m_new;
+        }
+        float ps[2] = {0.f, 0.f};
+#pragma unroll
+        for (int mt = 0; mt < C::kMT; ++mt) {
+#pragma unroll
+          for (int r = 0; r < 4; ++r) {
+            sc[mt][r] = exp2f(sc[mt][r] - m_run[r & 1]);
+            ps[r & 1] += sc[mt][r];
+          }
+        }
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          ps[e] += __shfl_xor_sync(0xffffffffu, ps[e], 4);
+          ps[e] += __shfl_xor_sync(0xffffffffu, ps[e], 8);
+          ps[e] += __shfl_xor_sync(0xffffffffu, ps[e], 16);
+          l_run[e] = l_run[e] * alpha[e] + ps[e];
+        }
+#pragma unroll
+        for (int dt = 0; dt < C::kDT; ++dt) {
+          o[dt][0] *= alpha[0];
+          o[dt][1] *= alpha[1];
+          o[dt][2] *= alpha[0];
+          o[dt][3] *= alpha[1];
+        }
+        // ---- O^T += V^T P^T : d (M) x heads (N), tokens as K ----
+#pragma unroll
+        for (int kk = 0; kk < C::kPK; ++kk) {
+          // P^T fragment of tokens 16kk..16kk+15 (b0: +0..7, b1: +8..15)
+          const uint32_t pb0 = movm_t(pack_bf16(sc[kk][0], sc[kk][1]));
+          const uint32_t pb1 = movm_t(pack_bf16(sc[kk][2], sc[kk][3]));
+          // V rows >= valid may hold never-written data: zero this thread's
+          // A-fragment halves for those tokens so 0 * garbage cannot poison O.
+          uint32_t vm0 = 0xffffffffu, vm1 = 0xffffffffu;
+          if (valid < B) {
+            const int t0 = 16 * kk + 2 * t;
+            vm0 = (t0 < valid ? 0x0000ffffu : 0u) | (t0 + 1 < valid ? 0xffff0000u : 0u);
+            vm1 = (t0 + 8 < valid ? 0x0000ffffu : 0u) | (t0 + 9 < valid ? 0xffff0000u : 0u);
+          }
+#pragma unroll
+          for (int dt = 0; dt < C::kDT; ++dt) {
+            uint32_t a[4];
+            ldsm_x4_t(swz<B>(vst, 16 * kk + lr + 8 * (lm >> 1), 2 * dt + (lm & 1)), a);
+            a[0] &= vm0;
+            a[1] &= vm0;
+            a[2] &= vm1;
+            a[3] &= vm1;
+            mma_bf16(o[dt], a, pb0, pb1);
+          }
+        }
       }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[stage]);
     }
-    float mx = fmaxf(fmaxf(sv[0], sv[1]), fmaxf(sv[2], sv[3]));
-    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
-    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
-    const float m_new = fmaxf(m_run, mx);
-    const float alpha = exp2f(m_run - m_new);
-    float p[4], ps = 0.f;
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      p[e] = exp2f(sv[e] - m_new);
-      ps += p[e];
-    }
-    ps += __shfl_xor_sync(0xffffffffu, ps, 1);
-    ps += __shfl_xor_sync(0xffffffffu, ps, 2);
-    l_run = l_run * alpha + ps;
-    m_run = m_new;
-#pragma unroll
-    for (int nt = 0; nt < C::kNT; ++nt) {
-      o[nt][0] *= alpha;
-      o[nt][1] *= alpha;
-    }
-    const uint32_t pa0 = pack_bf16(p[0], p[1]);
-    const uint32_t pa2 = pack_bf16(p[2], p[3]);
-    // ---- O += P V ----
-#pragma unroll
-    for (int np = 0; np < C::kNT / 2; ++np) {
-      uint32_t v[4];
-      ldsm_x4_t(swz(vst, ((mm & 1) << 3) + mr, 2 * np + (mm >> 1)), v);
-      mma_bf16(o[2 * np], pa0, 0u, pa2, 0u, v[0], v[1]);
-      mma_bf16(o[2 * np + 1], pa0, 0u, pa2, 0u, v[2], v[3]);
+    if (piece_end == u_end && warp == 0) trace(3, args.layer);
+
+    // ---- hand this warp's piece state to the merge slot ----
+    if (k == 0) pdl_wait();
+    if (lane == 0) {
+      while (ld_acquire_cta(&ctr[2]) != k) {
+      }
     }
     __syncwarp();
-    // refill this stage with the unit kStages ahead
-    if (k + C::kStages < n_units) {
-      if (lane == 0) {
-        fence_proxy_async();
-        issue(pu, stage);
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int hh = 2 * t + e;
+      if (hh < GQ) {
+        float* pr = stv + (warp * GQ + hh) * C::kRow;
+        if (g == 0) {
+          pr[HD] = m_run[e];
+          pr[HD + 1] = l_run[e];
+        }
+#pragma unroll
+        for (int dt = 0; dt < C::kDT; ++dt) {
+          pr[16 * dt + g] = o[dt][e];
+          pr[16 * dt + g + 8] = o[dt][2 + e];
+        }
       }
-      advance(pu);
     }
-
-    // ---- segment flush ----
-    const bool seg_end = (cu.j == cu.ups - 1) || (k == n_units - 1);
-    if (seg_end) {
-      const int64_t sb = cu.seg_begin, se = cu.seg_begin + cu.ups;
-      const bool whole = sb >= u_begin && se <= u_end;
-      const int sg = cu.s * H + cu.h;
-      const int64_t qrow = (int64_t)cu.s * args.out_stride + (int64_t)cu.h * GQ * HD;
+    __syncwarp();
+    int last = 0;
+    if (lane == 0) {
+      __threadfence_block();
+      last = atomicAdd(&ctr[1], 1) == kConsumers - 1;
+    }
+    last = __shfl_sync(0xffffffffu, last, 0);
+    if (last) {
+      // ---- this warp merges the piece (warp order, deterministic) ----
+      __threadfence_block();
+      const int hh = (lane * C::kEPL) / HD, el = (lane * C::kEPL) % HD;
+      float M = -INFINITY, L = 0.f, acc[C::kEPL];
+#pragma unroll
+      for (int e = 0; e < C::kEPL; ++e) acc[e] = 0.f;
+#pragma unroll
+      for (int w = 0; w < kConsumers; ++w) M = fmaxf(M, stv[(w * GQ + hh) * C::kRow + HD]);
+#pragma unroll
+      for (int w = 0; w < kConsumers; ++w) {
+        const float* pr = stv + (w * GQ + hh) * C::kRow;
+        const float f = pr[HD] == -INFINITY ? 0.f : exp2f(pr[HD] - M);
+        L = fmaf(pr[HD + 1], f, L);
+        if constexpr (C::kEPL % 4 == 0) {
+#pragma unroll
+          for (int e = 0; e < C::kEPL; e += 4) {
+            const float4 x = *reinterpret_cast<const float4*>(pr + el + e);
+            acc[e] = fmaf(x.x, f, acc[e]);
+            acc[e + 1] = fmaf(x.y, f, acc[e + 1]);
+            acc[e + 2] = fmaf(x.z, f, acc[e + 2]);
+            acc[e + 3] = fmaf(x.w, f, acc[e + 3]);
+          }
+        } else {
+#pragma unroll
+          for (int e = 0; e < C::kEPL; e += 2) {
+            const float2 x = *reinterpret_cast<const float2*>(pr + el + e);
+            acc[e] = fmaf(x.x, f, acc[e]);
+            acc[e + 1] = fmaf(x.y, f, acc[e + 1]);
+          }
+        }
+      }
+      // the slot is free again once the states are in registers
+      __syncwarp();
+      if (lane == 0) {
+        ctr[1] = 0;
+        st_release_cta(&ctr[2], k + 1);
+      }
+      const bool whole = seg_begin >= u_begin && seg_end <= u_end;
+      const int sg = s * H + h;
+      __nv_bfloat16* orow = args.out + (int64_t)s * args.out_stride + ((int64_t)h * GQ + hh) * HD + el;
+      float* lse = args.lse ? args.lse + (int64_t)s * d.q_heads + h * GQ + hh : nullptr;
       if (whole) {
-        if (g < GQ) {
-          const float inv = 1.f / l_run;
+        const float inv = 1.f / L;
 #pragma unroll
-          for (int nt = 0; nt < C::kNT; ++nt) {
-            *reinterpret_cast<__nv_bfloat162*>(args.out + qrow + g * HD + nt * 8 + 2 * t) =
-                __floats2bfloat162_rn(o[nt][0] * inv, o[nt][1] * inv);
-          }
-          if (args.lse && t == 0)
-            args.lse[(int64_t)cu.s * d.q_heads + cu.h * GQ + g] = (m_run + log2f(l_run)) * kLn2;
-        }
+        for (int e = 0; e < C::kEPL; e += 2)
+          *reinterpret_cast<__nv_bfloat162*>(orow + e) = __floats2bfloat162_rn(acc[e] * inv, acc[e + 1] * inv);
+        if (lse && el == 0) *lse = (M + log2f(L)) * kLn2;
       } else {
-        // partial slot (sg + gw): O [GQ][HD+4] (16-B aligned rows), m at +HD, l at +HD+1
-        constexpr int kRow = HD + 4;
-        float* slot = ws.attn_part + (int64_t)(sg + gw) * GQ * kRow;
-        if (g < GQ) {
+        // split segment: partial (2*cta + which), which = 0 for the CTA's first piece
+        const int which = (u == u_begin) ? 0 : 1;
+        float* slot = ws.attn_part + ((int64_t)(2 * c + which) * GQ + hh) * C::kRow;
 #pragma unroll
-          for (int nt = 0; nt < C::kNT; ++nt)
-            *reinterpret_cast<float2*>(slot + g * kRow + nt * 8 + 2 * t) = make_float2(o[nt][0], o[nt][1]);
-          if (t == 0) {
-            slot[g * kRow + HD] = m_run;
-            slot[g * kRow + HD + 1] = l_run;
-          }
+        for (int e = 0; e < C::kEPL; ++e) slot[el + e] = acc[e];
+        if (el == 0) {
+          slot[HD] = M;
+          slot[HD + 1] = L;
         }
+        int c_first, c_last;
+        if (kp > 0) {  // the segment's pieces sit on consecutive CTAs
+          const int ks = min(kp, (np + kMinPiece - 1) / kMinPiece);
+          c_first = ppre[s] + h * ks;
+          c_last = c_first + ks - 1;
+        } else {
+          c_first = (int)(((int64_t)(seg_begin + 1) * G + N - 1) / N) - 1;
+          c_last = (int)(((int64_t)seg_end * G + N - 1) / N) - 1;
+        }
+        fence_acq_rel_gpu();
         __syncwarp();
-        const int64_t w_first = ((sb + 1) * NW + N - 1) / N - 1;
-        const int64_t w_last = (se * NW + N - 1) / N - 1;
-        int last = 0;
-        if (lane == 0) {
-          __threadfence();
-          last = atomicAdd(&ws.attn_done[sg], 1) == (int)(w_last - w_first);
-        }
-        last = __shfl_sync(0xffffffffu, last, 0);
-        if (last) {
-          __threadfence();
-          // merge in warp order: per head M = max m_w, L = sum l_w 2^(m_w - M);
-          // each lane owns EPL consecutive elements of one head.
-          const float* base = ws.attn_part + (sg + w_first) * GQ * kRow;
-          const int nsl = (int)(w_last - w_first + 1);
-          float M[GQ], L[GQ];
+        int fin = 0;
+        if (lane == 0) fin = atomicAdd(&ws.attn_done[sg], 1) == (c_last - c_first);
+        fin = __shfl_sync(0xffffffffu, fin, 0);
+        if (fin) {
+          fence_acq_rel_gpu();
+          // pieces in chunks whose loads are all in flight together
+          constexpr int kPieces = C::kEPL >= 32 ? 2 : (C::kEPL >= 16 ? 4 : 8);
+          const int npieces = c_last - c_first + 1;
+          float Mx = -INFINITY, Lx = 0.f, ax[C::kEPL];
 #pragma unroll
-          for (int gg = 0; gg < GQ; ++gg) {
-            float mx = -INFINITY;
-            for (int w2 = lane; w2 < nsl; w2 += 32) mx = fmaxf(mx, __ldcg(base + (int64_t)w2 * GQ * kRow + gg * kRow + HD));
+          for (int e = 0; e < C::kEPL; ++e) ax[e] = 0.f;
+          for (int p0c = 0; p0c < npieces; p0c += kPieces) {
+            float mv[kPieces], lv[kPieces], xv[kPieces][C::kEPL];
 #pragma unroll
-            for (int o2 = 16; o2 >= 1; o2 >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o2));
-            float sum = 0.f;
-            for (int w2 = lane; w2 < nsl; w2 += 32) {
-              const float* sl = base + (int64_t)w2 * GQ * kRow + gg * kRow;
-              sum += __ldcg(sl + HD + 1) * exp2f(__ldcg(sl + HD) - mx);
+            for (int q = 0; q < kPieces; ++q) {
+              mv[q] = -INFINITY;
+              lv[q] = 0.f;
+              if (p0c + q < npieces) {
+                const int cc = c_first + p0c + q;
+                const int ub = (int)((int64_t)cc * N / G);
+                const int wh = (kp > 0 || max(seg_begin, ub) == ub) ? 0 : 1;
+                const float* pr = ws.attn_part + ((int64_t)(2 * cc + wh) * GQ + hh) * C::kRow;
+                const float2 ml = __ldcg(reinterpret_cast<const float2*>(pr + HD));
+                mv[q] = ml.x;
+                lv[q] = ml.y;
+#pragma unroll
+                for (int e = 0; e < C::kEPL; e += 2) {
+                  const float2 x = __ldcg(reinterpret_cast<const float2*>(pr + el + e));
+                  xv[q][e] = x.x;
+                  xv[q][e + 1] = x.y;
+                }
+              }
             }
+            float Mn = Mx;
 #pragma unroll
-            for (int o2 = 16; o2 >= 1; o2 >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o2);
-            M[gg] = mx;
-            L[gg] = sum;
-          }
-          constexpr int kEPL = GQ * HD / 32;
-          const int e0 = lane * kEPL;
-          const int gl = e0 / HD, el = e0 - gl * HD;
-          float Mg = M[0], Lg = L[0];
+            for (int q = 0; q < kPieces; ++q) Mn = fmaxf(Mn, mv[q]);
+            const float rs = Mx == -INFINITY ? 0.f : exp2f(Mx - Mn);
+            Lx *= rs;
 #pragma unroll
-          for (int gg = 1; gg < GQ; ++gg)
-            if (gl == gg) { Mg = M[gg]; Lg = L[gg]; }
-          float acc[kEPL];
+            for (int e = 0; e < C::kEPL; ++e) ax[e] *= rs;
+            Mx = Mn;
 #pragma unroll
-          for (int e = 0; e < kEPL; ++e) acc[e] = 0.f;
-          for (int w2 = 0; w2 < nsl; ++w2) {
-            const float* sl = base + (int64_t)w2 * GQ * kRow + gl * kRow;
-            const float f = exp2f(__ldcg(sl + HD) - Mg);
+            for (int q = 0; q < kPieces; ++q) {
+              const float f = mv[q] == -INFINITY ? 0.f : exp2f(mv[q] - Mx);
+              Lx = fmaf(lv[q], f, Lx);
 #pragma unroll
-            for (int e = 0; e < kEPL; e += 2) {
-              const float2 x = __ldcg(reinterpret_cast<const float2*>(sl + el + e));
-              acc[e] = fmaf(x.x, f, acc[e]);
-              acc[e + 1] = fmaf(x.y, f, acc[e + 1]);
+              for (int e = 0; e < C::kEPL; ++e) ax[e] = fmaf(p0c + q < npieces ? xv[q][e] : 0.f, f, ax[e]);
             }
           }
-          const float inv = 1.f / Lg;
+          const float inv = 1.f / Lx;
 #pragma unroll
-          for (int e = 0; e < kEPL; e += 2)
-            *reinterpret_cast<__nv_bfloat162*>(args.out + qrow + gl * HD + el + e) =
-                __floats2bfloat162_rn(acc[e] * inv, acc[e + 1] * inv);
-          if (args.lse && el == 0)
-            args.lse[(int64_t)cu.s * d.q_heads + cu.h * GQ + gl] = (Mg + log2f(Lg)) * kLn2;
+          for (int e = 0; e < C::kEPL; e += 2)
+            *reinterpret_cast<__nv_bfloat162*>(orow + e) = __floats2bfloat162_rn(ax[e] * inv, ax[e + 1] * inv);
+          if (lse && el == 0) *lse = (Mx + log2f(Lx)) * kLn2;
           if (lane == 0) ws.attn_done[sg] = 0;
         }
       }
-      advance(cu);
-      if (k + 1 < n_units) load_q(cu);
-    } else {
-      advance(cu);
     }
+    u = piece_end;
+    ++k;
   }
+  // exit stamp: the last consumer warp to finish (merges included)
+  if (lane == 0 && blockIdx.x < 256) atomicMax(&g_attn_trace[args.layer & 1][blockIdx.x][4], (unsigned long long)global_ns());
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
@@ -450,15 +691,15 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
-// 3-D view [layers][n_phys*kv_heads*page][head_dim] of a KV pool; 8-row x
-// 64-column boxes with 128-byte swizzle.
+// 3-D view [layers][n_phys*kv_heads*page][head_dim] of a KV pool; boxes of
+// 64 columns x one page of rows with 128-byte swizzle.
 int make_kv_map(CUtensorMap* m, const void* base, const ChessDims& d) {
   auto fn = encode_fn();
   if (!fn) return fail(CHESS_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
   const cuuint64_t rows = (cuuint64_t)d.n_phys * d.kv_heads * d.page_size;
   cuuint64_t dims[3] = {(cuuint64_t)d.head_dim, rows, (cuuint64_t)d.layers};
   cuuint64_t strides[2] = {(cuuint64_t)d.head_dim * 2, rows * d.head_dim * 2};
-  cuuint32_t box[3] = {64, 8, 1};
+  cuuint32_t box[3] = {64, (cuuint32_t)d.page_size, 1};
   cuuint32_t es[3] = {1, 1, 1};
   CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box,
                   es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -492,7 +733,8 @@ int launch_inst(const ChessState& st, const Workspace& ws, const AttnArgs& args,
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  static const bool no_pdl = getenv("CHESS_ATTN_NOPDL") != nullptr;  // debug A/B
+  cfg.numAttrs = no_pdl ? 0 : 1;
   cudaLaunchKernelEx(&cfg, kfn, st, ws, args, km, vm);
   return check_launch("sparse_decode");
 }
@@ -516,8 +758,14 @@ int launch_sparse_decode(const ChessState& st, const Workspace& ws, int layer, c
   a.lse = lse;
   a.scale_log2 = softmax_scale * kLog2e;
   a.layer = layer;
+  static const int dbg_mode = getenv("CHESS_ATTN_MODE") ? atoi(getenv("CHESS_ATTN_MODE")) : 0;
+  a.mode = dbg_mode;
   const int gq = d.q_heads / d.kv_heads;
   const int nctas = ws.attn_ctas;
+  if ((reinterpret_cast<uintptr_t>(q) & 15) || (q_stride & 7))
+    return fail(CHESS_ERR_UNSUPPORTED, "sparse_decode: q must be 16-byte aligned with q_stride %% 8 == 0");
+  if (d.kv_heads > 255 || d.batch > (1 << 22))
+    return fail(CHESS_ERR_UNSUPPORTED, "sparse_decode: kv_heads must be <= 255");
 #define CHESS_ATTN_CASE(HD_, GQ_, B_)                                        \
   if (d.head_dim == HD_ && gq == GQ_ && d.page_size == B_)                   \
     return launch_inst<HD_, GQ_, B_>(st, ws, a, nctas, stream);
@@ -527,8 +775,10 @@ int launch_sparse_decode(const ChessState& st, const Workspace& ws, int layer, c
   CHESS_ATTN_CASE(128, 8, 16)
   CHESS_ATTN_CASE(128, 1, 32)
   CHESS_ATTN_CASE(128, 1, 16)
+  CHESS_ATTN_CASE(128, 2, 32)
   CHESS_ATTN_CASE(64, 1, 16)
   CHESS_ATTN_CASE(64, 1, 32)
+  CHESS_ATTN_CASE(64, 2, 16)
   CHESS_ATTN_CASE(64, 4, 16)
   CHESS_ATTN_CASE(64, 4, 32)
   CHESS_ATTN_CASE(64, 8, 32)
@@ -538,3 +788,9 @@ int launch_sparse_decode(const ChessState& st, const Workspace& ws, int layer, c
 }
 
 }  // namespace chess
+
+// Debug only (not part of include/chess_b200.h): copy the per-CTA timeline of
+// the last sparse_decode launch of each layer parity, [2][256][8] u64 ns.
+extern "C" int chess_debug_attn_trace(unsigned long long* host_out) {
+  return cudaMemcpyFromSymbol(host_out, chess::g_attn_trace, sizeof(chess::g_attn_trace)) == cudaSuccess ? 0 : 8;
+}

@@ -158,13 +158,13 @@ __global__ void __launch_bounds__(kNT) entropy_kernel(ChessState st, Workspace w
     part[0] = (double)M;
     part[1] = Sb;
     part[2] = Tb;
-    __threadfence();
+    fence_acq_rel_gpu();
     const int prev = atomicAdd(&ws.ent_done[r], 1);
     s_last = (prev == nsplit - 1);
   }
   __syncthreads();
   if (!s_last || threadIdx.x != 0) return;
-  __threadfence();
+  fence_acq_rel_gpu();
   ws.ent_done[r] = 0;
   double Mt = 0.0, St = 0.0, Tt = 0.0;
   for (int q = 0; q < nsplit; ++q) {

@@ -162,13 +162,13 @@ __global__ void __launch_bounds__(kNT) append_kernel(ChessState st, const __nv_b
   // pre-state above before incrementing).
   __syncthreads();
   if (threadIdx.x == 0) {
-    __threadfence();
+    fence_acq_rel_gpu();
     const int prev = atomicAdd(&done[s], 1);
     s_last = (prev == (int)gridDim.x - 1);
   }
   __syncthreads();
   if (!s_last) return;
-  __threadfence();
+  fence_acq_rel_gpu();
   if (threadIdx.x == 0) {
     done[s] = 0;
     st.num_pages[s] = open_new ? np + 1 : np;
@@ -222,7 +222,7 @@ __global__ void __launch_bounds__(kNT) seal_kernel(ChessState st, int32_t* done)
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-    __threadfence();
+    fence_acq_rel_gpu();
     const int prev = atomicAdd(&done[s], 1);
     s_last = (prev == (int)gridDim.x - 1);
   }
@@ -290,7 +290,7 @@ __global__ void __launch_bounds__(kNT) fold_rows_kernel(ChessState st, int s, co
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-    __threadfence();
+    fence_acq_rel_gpu();
     const int prev = atomicAdd(&done[s], 1);
     s_last = (prev == (int)gridDim.x - 1);
   }

@@ -354,14 +354,14 @@ __global__ void __launch_bounds__(kScanCTA, 1) select_scan_kernel(ChessState st,
     // one release per (CTA, slot) run: publishes this CTA's partials
     block_sync<kNT>();
     if (threadIdx.x == 0) {
-      __threadfence();
+      fence_acq_rel_gpu();
       const int items_s = s_prefix[s_done + 1] - s_prefix[s_done];
       const int prev = atomicAdd(&ws.sel_done[s_done], contributed);
       s_last = (prev + contributed == items_s);
     }
     block_sync<kNT>();
     if (s_last) {
-      __threadfence();
+      fence_acq_rel_gpu();
       select_tail(st, ws, prm, s_done, level, level_rows(st, ws, prm, s_done, level), sm);
       if (threadIdx.x == 0) ws.sel_done[s_done] = 0;
       block_sync<kNT>();
