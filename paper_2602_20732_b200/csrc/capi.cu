@@ -4,6 +4,7 @@
 // selection.py:55-56/68-72, hierarchy.py:108-114, kv_store.py:161-164); every
 // check happens before launch, no entry point synchronises its stream.
 #include <cstdarg>
+#include <cstdlib>
 #include <mutex>
 
 #include "common.cuh"
@@ -88,7 +89,7 @@ static size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 size_t workspace_layout(const ChessDims& d, void* base, Workspace* ws) {
   const int64_t b = d.batch;
   const int64_t mr = max_rows(d);
-  const int64_t nsl = (d.ld + kScanSlice - 1) / kScanSlice;
+  const int64_t nsl = (d.ld + scan_slice(d.summary_dtype) - 1) / scan_slice(d.summary_dtype);
   const int64_t gq = d.kv_heads > 0 ? d.q_heads / d.kv_heads : 1;
   const int64_t attn_slots = b * d.kv_heads + kAttnWarpsMax;
   size_t off = 0;
@@ -272,6 +273,8 @@ int chess_select(const ChessState* st, const ChessSelectCfg* cfg, void* stream) 
   prm.rho[1] = r[1];
   prm.rho[2] = r[2];
   prm.full_scan = cfg->full_scan;
+  static const int dbg_mode = getenv("CHESS_SELECT_MODE") ? atoi(getenv("CHESS_SELECT_MODE")) : 0;
+  prm.mode = dbg_mode;
   prm.force_all = cfg->force_all;
   const int grid = 4 * num_sms();
   return launch_select(*st, ws, prm, grid, (cudaStream_t)stream);

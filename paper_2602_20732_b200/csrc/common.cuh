@@ -38,7 +38,11 @@ __host__ __device__ inline int64_t max_rows(const ChessDims& d) { return d.max_p
 // ---------------------------------------------------------------------------
 // workspace layout (carved from ChessState::workspace, see capi.cu)
 // ---------------------------------------------------------------------------
-constexpr int kScanSlice = 2048;   // elements of one (row, slice) work unit
+// Elements of one (row, slice) scan work unit: 16 KB of summary row per
+// bulk copy (f32 mirrors: 4096, f64 rows: 2048), so a ring of 12 stages
+// holds 1.5 items of 8 rows.
+constexpr int kScanSliceBytes = 16384;
+__host__ __device__ constexpr int scan_slice(int summary_dtype) { return summary_dtype == 0 ? kScanSliceBytes / 4 : kScanSliceBytes / 8; }
 constexpr int kScanRows = 8;       // rows per work item
 constexpr int kScanThreads = 256;
 constexpr int kMaxBatch = 1024;
@@ -72,6 +76,7 @@ struct SelParams {
   double rho[3];
   int32_t full_scan;
   int32_t force_all;
+  int32_t mode;  // debug (CHESS_SELECT_MODE): 0 normal, 1 no math, 2 no loads
 };
 
 // ---------------------------------------------------------------------------
@@ -234,6 +239,19 @@ __device__ __forceinline__ void tma_load_1d(void* dst_smem, const void* src_gmem
 // cheaper than __threadfence() (fence.sc.gpu + L1 invalidate, SASS ERRBAR +
 // CCTL.IVALL), which showed up as microseconds per split-K merge.
 __device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+
+// explicit shared-window vector loads (a generic pointer into dynamic smem
+// after alignment arithmetic compiles to LD.E, not LDS)
+__device__ __forceinline__ float4 lds_f4(uint32_t a) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ double2 lds_d2(uint32_t a) {
+  double2 v;
+  asm volatile("ld.shared.v2.f64 {%0,%1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(a));
+  return v;
+}
 
 // Programmatic dependent launch controls (griddepcontrol, sm_90+).
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }

@@ -13,7 +13,7 @@
 // output-identical to Alg.1's full scan (a masked top-k can never keep a
 // child of a pruned parent); `full_scan` keeps the literal one-GEMV variant.
 //
-// Work decomposition: an item is (slot, 8 candidate rows, 2048-element slice).
+// Work decomposition: an item is (slot, 8 candidate rows, 16 KB row slice).
 // Persistent CTAs stride over items; per-(row, slice) partials land in the
 // workspace and the last CTA to finish a slot's items (atomic counter) reduces
 // them in fixed slice order (deterministic), runs the radix top-k and writes
@@ -102,9 +102,19 @@ __device__ __forceinline__ const double* level_row_ptr<double>(const ChessState&
 // ---------------------------------------------------------------------------
 // tail: reduce partials, top-k, emit next level (block-wide, one slot)
 // ---------------------------------------------------------------------------
+constexpr int kTailCap = 1024;  // candidates whose keys / flags stay in shared memory
+
+// Debug: per slot of the last launch of each level, tail timeline
+// {flush entered, counter won, scores reduced, level-0 top-k, done}.
+__device__ unsigned long long g_tail_trace[4][64][8];
+__device__ __forceinline__ void tail_trace(int level, int s, int which) {
+  if (threadIdx.x == 0 && s < 64) g_tail_trace[level][s][which] = global_ns();
+}
 struct TailSmem {
   int hist[256];
   int scratch[64];
+  uint64_t keys[kTailCap];
+  int kept[kTailCap];
 };
 
 __device__ void expand_children(const int* parents, int m, int fan, int total_children, int* out,
@@ -128,20 +138,37 @@ __device__ void select_tail(const ChessState& st, const Workspace& ws, const Sel
   const int64_t mr = max_rows(d);
   const int ns = ws.n_slices;
   double* sc = ws.scores + (int64_t)s * mr;
-  uint64_t* keys = ws.keys + (int64_t)s * mr;
-  int* kept = ws.kept + (int64_t)s * mr;
+  // keys / kept flags of every level pass fit in smem unless the full-scan
+  // candidate count is large
+  const bool in_smem = n <= kTailCap;  // n bounds every level's candidate count
+  uint64_t* keys = in_smem ? sm.keys : ws.keys + (int64_t)s * mr;
+  int* kept = in_smem ? sm.kept : ws.kept + (int64_t)s * mr;
   int* plist = ws.plist + (int64_t)s * mr;
   const double* part = ws.part + (int64_t)s * mr * ns;
   const LevelShape sh = shape_of(st, s);
   int* stats = st.sel_stats + 8 * s;
 
-  // fixed-order reduction over slices (deterministic)
+  // fixed-order reduction over slices (deterministic); the slice partials of
+  // a row are loaded together (one round trip) when ns <= 16
   for (int i = threadIdx.x; i < n; i += kNT) {
-    double acc = __ldcg(part + (int64_t)i * ns);
-    for (int q = 1; q < ns; ++q) acc = __dadd_rn(acc, __ldcg(part + (int64_t)i * ns + q));
+    const double* pr = part + (int64_t)i * ns;
+    double acc;
+    if (ns <= 16) {
+      double v[16];
+#pragma unroll
+      for (int q = 0; q < 16; ++q) v[q] = q < ns ? __ldcg(pr + q) : 0.0;
+      acc = v[0];
+#pragma unroll
+      for (int q = 1; q < 16; ++q)
+        if (q < ns) acc = __dadd_rn(acc, v[q]);
+    } else {
+      acc = __ldcg(pr);
+      for (int q = 1; q < ns; ++q) acc = __dadd_rn(acc, __ldcg(pr + q));
+    }
     sc[i] = acc;
   }
   block_sync<kNT>();
+  tail_trace(level, s, 2);
 
   // level order to run in this tail
   const int lv_begin = level == 3 ? 0 : level;
@@ -174,6 +201,7 @@ __device__ void select_tail(const ChessState& st, const Workspace& ws, const Sel
     // ceil in double (selection.py:98, 103, 108)
     const int k = (int)ceil(prm.rho[lv] * (double)m);
     block_topk_mark<kNT>(keys, m, k, kept, sm.hist, sm.scratch);
+    if (lv == lv_begin) tail_trace(level, s, 3);
     const int fan = lv == 0 ? d.chunks_per_grid : d.pages_per_chunk;
     int kcount;
     if (lv < 2) {
@@ -223,8 +251,8 @@ __device__ void handle_empty_slots(const ChessState& st, const Workspace& ws, co
 // ---------------------------------------------------------------------------
 // the scan kernel (one launch per level; level 3 = Alg.1 full scan)
 //
-// Warp 8 is a TMA producer: one cp.async.bulk per (candidate row, 2048-element
-// slice) into a 128 KB shared-memory ring (16 x 8 KB stages for f32 rows).
+// Warp 8 is a TMA producer: one cp.async.bulk per (candidate row, 16 KB
+// slice) into a 192 KB shared-memory ring (12 x 16 KB stages).
 // Warps 0-7 consume: each thread owns 8 elements of the slice (conflict-free
 // 16-byte LDS), multiplies by its f64 anchor registers, and the 8 row
 // partials of an item are transpose-reduced across the warp and then across
@@ -233,12 +261,22 @@ __device__ void handle_empty_slots(const ChessState& st, const Workspace& ws, co
 // ---------------------------------------------------------------------------
 constexpr int kScanCTA = kNT + 32;  // 8 consumer warps + 1 producer warp
 
+// Debug timeline (chess_debug_select_trace): per CTA of the last launch of
+// each level, {entry, prologue, first row, items done, exit, wait cycles of
+// warp 0, rows consumed}.
+__device__ unsigned long long g_sel_trace[4][256][8];
+__device__ __forceinline__ void sel_trace(int level, int which, unsigned long long v) {
+  if (blockIdx.x < 256) g_sel_trace[level][blockIdx.x][which] = v;
+}
+
 template <typename T>
 struct ScanCfg {
-  static constexpr int kStageBytes = kScanSlice * (int)sizeof(T);
-  static constexpr int kStages = (128 * 1024) / kStageBytes;
+  static constexpr int kSlice = kScanSliceBytes / (int)sizeof(T);   // elements per row slice
+  static constexpr int kStageBytes = kScanSliceBytes;
+  static constexpr int kStages = (192 * 1024) / kStageBytes;
   static constexpr int kVec = 16 / (int)sizeof(T);                // elements per 16-B chunk
-  static constexpr int kGroups = 8 / kVec;                         // chunks per thread
+  static constexpr int kPerThread = kSlice / kNT;                  // elements per thread
+  static constexpr int kGroups = kPerThread / kVec;                // chunks per thread
   __device__ static int off(int v) { return (v * kNT + (int)threadIdx.x) * kVec; }
 };
 
@@ -251,6 +289,7 @@ __global__ void __launch_bounds__(kScanCTA, 1) select_scan_kernel(ChessState st,
   uint64_t* full = reinterpret_cast<uint64_t*>(ring + (size_t)SC::kStages * SC::kStageBytes);
   uint64_t* empty = full + SC::kStages;
   int* s_prefix = reinterpret_cast<int*>(empty + SC::kStages);  // [batch + 1]
+  int* s_rows = s_prefix + kMaxBatch + 1;                        // [batch] candidate rows
   __shared__ double s_wpart[2][kScanRows][kWarps];
   __shared__ TailSmem sm;
   __shared__ int s_last;
@@ -258,6 +297,12 @@ __global__ void __launch_bounds__(kScanCTA, 1) select_scan_kernel(ChessState st,
   const int nb = d.batch;
   const int nsl = ws.n_slices;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) {
+    sel_trace(level, 0, global_ns());
+    sel_trace(level, 5, 0);
+    sel_trace(level, 6, 0);
+    sel_trace(level, 7, 0);
+  }
 
   // per-slot item counts -> prefix (warp 0), barrier init (lane 0)
   if (warp == 0) {
@@ -267,6 +312,7 @@ __global__ void __launch_bounds__(kScanCTA, 1) select_scan_kernel(ChessState st,
       int items = 0;
       if (s < nb) {
         const int n = level_rows(st, ws, prm, s, level);
+        s_rows[s] = n;
         items = ((n + kScanRows - 1) / kScanRows) * nsl;
       }
       int incl = items;
@@ -288,6 +334,7 @@ __global__ void __launch_bounds__(kScanCTA, 1) select_scan_kernel(ChessState st,
     }
   }
   __syncthreads();
+  if (threadIdx.x == 0) sel_trace(level, 1, global_ns());
   // contiguous item range per CTA; within a slot items are ordered
   // (slice, row block) so a CTA reuses one anchor slice across row blocks.
   const int total = s_prefix[nb];
@@ -307,7 +354,7 @@ __global__ void __launch_bounds__(kScanCTA, 1) select_scan_kernel(ChessState st,
   auto decode = [&](int it, int s) {
     ItemPos p;
     p.s = s;
-    p.n = level_rows(st, ws, prm, s, level);
+    p.n = s_rows[s];
     const int nrb = (p.n + kScanRows - 1) / kScanRows;
     const int local = it - s_prefix[s];
     p.slice = local / nrb;
@@ -319,27 +366,76 @@ __global__ void __launch_bounds__(kScanCTA, 1) select_scan_kernel(ChessState st,
 
   if (warp == kWarps) {
     // ===================== TMA producer =====================
-    if (lane == 0) {
-      int k = 0;
-      int s = -1;
-      LevelShape sh{};
-      for (int it = it_begin; it < it_end; ++it) {
-        if (s < 0 || it >= s_prefix[s + 1]) {
-          s = slot_of(it);
-          sh = shape_of(st, s);
-        }
+    // Ops are (item, row) pairs, 8 per item (rows past the item's count are
+    // skipped).  The 32 lanes resolve the source rows of 4 items with one
+    // coalesced round of candidate-id loads, prefetched one batch ahead, and
+    // lane 0 then issues their bulk copies back to back.
+    const int n_ops = (it_end - it_begin) * kScanRows;
+    auto fetch = [&](int base, const T*& src, uint32_t& bytes) {
+      src = nullptr;
+      bytes = 0;
+      const int op = base + lane;
+      if (op < n_ops) {
+        const int it = it_begin + op / kScanRows;
+        const int r = op % kScanRows;
+        const int s = slot_of(it);
         const ItemPos p = decode(it, s);
-        const int64_t ebase = (int64_t)p.slice * kScanSlice;
-        const uint32_t bytes = (uint32_t)(min((int64_t)kScanSlice, d.ld - ebase) * sizeof(T));
-        for (int r = 0; r < p.rows; ++r, ++k) {
-          const int stage = k % SC::kStages;
-          const uint32_t ph = (uint32_t)((k / SC::kStages) & 1);
-          mbar_wait(&empty[stage], ph ^ 1u);
-          mbar_arrive_expect_tx(&full[stage], bytes);
-          tma_load_1d(ring + (size_t)stage * SC::kStageBytes,
-                      level_row_ptr<T>(st, ws, s, level, p.r0 + r, sh) + ebase, bytes, &full[stage]);
+        if (r < p.rows) {
+          const LevelShape sh = shape_of(st, s);
+          const int64_t ebase = (int64_t)p.slice * SC::kSlice;
+          bytes = (uint32_t)(min((int64_t)SC::kSlice, d.ld - ebase) * sizeof(T));
+          src = level_row_ptr<T>(st, ws, s, level, p.r0 + r, sh) + ebase;
         }
       }
+    };
+    const T* cur_src;
+    uint32_t cur_bytes;
+    const T* nxt_src = nullptr;
+    uint32_t nxt_bytes = 0;
+    long long t_fetch = 0, t_issue = 0, t_wait = 0;
+    long long tq = clock64();
+    fetch(0, cur_src, cur_bytes);
+    int k = 0;
+    for (int base = 0; base < n_ops; base += 32) {
+      if (base + 32 < n_ops) fetch(base + 32, nxt_src, nxt_bytes);
+      const long long tq1 = clock64();
+      t_fetch += tq1 - tq;
+      tq = tq1;
+      // 4 items per batch; the lanes of an item issue their rows in parallel
+      const uint32_t valid = __ballot_sync(0xffffffffu, cur_bytes != 0);
+#pragma unroll 1
+      for (int q = 0; q < 4; ++q) {
+        const uint32_t grp = (valid >> (8 * q)) & 0xffu;
+        if (grp == 0) continue;
+        const int r = lane - 8 * q;
+        if (r >= 0 && r < 8 && ((grp >> r) & 1u)) {
+          const int kr = k + r;
+          const int stage = kr % SC::kStages;
+          const uint32_t ph = (uint32_t)((kr / SC::kStages) & 1);
+          const long long tw = clock64();
+          mbar_wait(&empty[stage], ph ^ 1u);
+          if (r == 0) t_wait += clock64() - tw;
+          if (prm.mode == 2) {
+            mbar_arrive(&full[stage]);
+          } else {
+            mbar_arrive_expect_tx(&full[stage], cur_bytes);
+            tma_load_1d(ring + (size_t)stage * SC::kStageBytes, cur_src, cur_bytes, &full[stage]);
+          }
+        }
+        k += __popc(grp);
+        __syncwarp();
+      }
+      const long long tq2 = clock64();
+      t_issue += tq2 - tq;
+      tq = tq2;
+      cur_src = nxt_src;
+      cur_bytes = nxt_bytes;
+    }
+    t_wait = __shfl_sync(0xffffffffu, t_wait, 0);
+    if (lane == 0) {
+      sel_trace(level, 5, t_fetch);
+      sel_trace(level, 6, t_issue);
+      sel_trace(level, 7, t_wait);
     }
     return;
   }
@@ -348,10 +444,12 @@ __global__ void __launch_bounds__(kScanCTA, 1) select_scan_kernel(ChessState st,
   if ((level == 0 || level == 3) && blockIdx.x == 0) handle_empty_slots(st, ws, prm, sm);
   int k = 0, buf = 0;
   int s = -1, contributed = 0, a_slice = -1;
-  double a[8];
+  double a[SC::kPerThread];
   bool in[SC::kGroups];
+  bool all_in = true;
   auto flush = [&](int s_done) {
     // one release per (CTA, slot) run: publishes this CTA's partials
+    const unsigned long long tf = global_ns();
     block_sync<kNT>();
     if (threadIdx.x == 0) {
       fence_acq_rel_gpu();
@@ -362,7 +460,10 @@ __global__ void __launch_bounds__(kScanCTA, 1) select_scan_kernel(ChessState st,
     block_sync<kNT>();
     if (s_last) {
       fence_acq_rel_gpu();
-      select_tail(st, ws, prm, s_done, level, level_rows(st, ws, prm, s_done, level), sm);
+      if (threadIdx.x == 0 && s_done < 64) g_tail_trace[level][s_done][0] = tf;
+      tail_trace(level, s_done, 1);
+      select_tail(st, ws, prm, s_done, level, s_rows[s_done], sm);
+      tail_trace(level, s_done, 4);
       if (threadIdx.x == 0) ws.sel_done[s_done] = 0;
       block_sync<kNT>();
     }
@@ -375,11 +476,12 @@ __global__ void __launch_bounds__(kScanCTA, 1) select_scan_kernel(ChessState st,
       a_slice = -1;
     }
     const ItemPos p = decode(it, s);
-    const int64_t ebase = (int64_t)p.slice * kScanSlice;
+    const int64_t ebase = (int64_t)p.slice * SC::kSlice;
     if (p.slice != a_slice) {  // anchor slice (f64) in registers; zero beyond ld
       a_slice = p.slice;
       const double* anc = st.anchor + (int64_t)s * d.ld + ebase;
 #pragma unroll
+      all_in = ebase + SC::kSlice <= d.ld;
       for (int v = 0; v < SC::kGroups; ++v) {
         const int o = SC::off(v);
         in[v] = ebase + o < d.ld;
@@ -392,37 +494,75 @@ __global__ void __launch_bounds__(kScanCTA, 1) select_scan_kernel(ChessState st,
         }
       }
     }
+    // all rows of the item first, then 8 independent dot-product chains
     double acc[kScanRows];
 #pragma unroll
     for (int r = 0; r < kScanRows; ++r) {
       acc[r] = 0.0;
       if (r < p.rows) {
-        const int stage = k % SC::kStages;
-        mbar_wait(&full[stage], (uint32_t)((k / SC::kStages) & 1));
-        const T* row = reinterpret_cast<const T*>(ring + (size_t)stage * SC::kStageBytes);
-        double x = 0.0;
+        const int kr = k + r;
+        mbar_wait(&full[kr % SC::kStages], (uint32_t)((kr / SC::kStages) & 1));
+        if (kr == 0 && threadIdx.x == 0) sel_trace(level, 2, global_ns());
+      }
+    }
+    if (prm.mode != 1) {
+      // shared-window addresses of the item's rows (explicit ld.shared)
+      uint32_t rowa[kScanRows];
+#pragma unroll
+      for (int r = 0; r < kScanRows; ++r)
+        rowa[r] = smem_u32(ring) + (uint32_t)(((k + r) % SC::kStages) * SC::kStageBytes);
+      if (p.rows == kScanRows && all_in) {
+        // fast path: full item, full slice — no predication
 #pragma unroll
         for (int v = 0; v < SC::kGroups; ++v) {
-          if (in[v]) {
+#pragma unroll
+          for (int r = 0; r < kScanRows; ++r) {
+            const uint32_t ad = rowa[r] + (uint32_t)(SC::off(v) * sizeof(T));
             if constexpr (sizeof(T) == 4) {
-              const float4 f = *reinterpret_cast<const float4*>(row + SC::off(v));
-              x = __fma_rn(a[4 * v + 0], (double)f.x, x);
-              x = __fma_rn(a[4 * v + 1], (double)f.y, x);
-              x = __fma_rn(a[4 * v + 2], (double)f.z, x);
-              x = __fma_rn(a[4 * v + 3], (double)f.w, x);
+              const float4 f = lds_f4(ad);
+              acc[r] = __fma_rn(a[4 * v + 0], (double)f.x, acc[r]);
+              acc[r] = __fma_rn(a[4 * v + 1], (double)f.y, acc[r]);
+              acc[r] = __fma_rn(a[4 * v + 2], (double)f.z, acc[r]);
+              acc[r] = __fma_rn(a[4 * v + 3], (double)f.w, acc[r]);
             } else {
-              const double2 f = *reinterpret_cast<const double2*>(row + SC::off(v));
-              x = __fma_rn(a[2 * v + 0], f.x, x);
-              x = __fma_rn(a[2 * v + 1], f.y, x);
+              const double2 f = lds_d2(ad);
+              acc[r] = __fma_rn(a[2 * v + 0], f.x, acc[r]);
+              acc[r] = __fma_rn(a[2 * v + 1], f.y, acc[r]);
             }
           }
         }
-        acc[r] = x;
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[stage]);
-        ++k;
+      } else {
+#pragma unroll
+        for (int v = 0; v < SC::kGroups; ++v) {
+          if (in[v]) {
+#pragma unroll
+            for (int r = 0; r < kScanRows; ++r) {
+              if (r < p.rows) {
+                const uint32_t ad = rowa[r] + (uint32_t)(SC::off(v) * sizeof(T));
+                if constexpr (sizeof(T) == 4) {
+                  const float4 f = lds_f4(ad);
+                  acc[r] = __fma_rn(a[4 * v + 0], (double)f.x, acc[r]);
+                  acc[r] = __fma_rn(a[4 * v + 1], (double)f.y, acc[r]);
+                  acc[r] = __fma_rn(a[4 * v + 2], (double)f.z, acc[r]);
+                  acc[r] = __fma_rn(a[4 * v + 3], (double)f.w, acc[r]);
+                } else {
+                  const double2 f = lds_d2(ad);
+                  acc[r] = __fma_rn(a[2 * v + 0], f.x, acc[r]);
+                  acc[r] = __fma_rn(a[2 * v + 1], f.y, acc[r]);
+                }
+              }
+            }
+          }
+        }
       }
     }
+    __syncwarp();
+    if (lane == 0) {
+#pragma unroll
+      for (int r = 0; r < kScanRows; ++r)
+        if (r < p.rows) mbar_arrive(&empty[(k + r) % SC::kStages]);
+    }
+    k += p.rows;
     // warp transpose-reduce of 8 row partials: 4+2+1 exchanges, then 2 xor adds.
     {
       const bool b4 = lane & 16;
@@ -460,7 +600,9 @@ __global__ void __launch_bounds__(kScanCTA, 1) select_scan_kernel(ChessState st,
     buf ^= 1;
     ++contributed;
   }
+  if (threadIdx.x == 0) sel_trace(level, 3, global_ns());
   if (s >= 0) flush(s);
+  if (threadIdx.x == 0) sel_trace(level, 4, global_ns());
 }
 
 // ---------------------------------------------------------------------------
@@ -653,11 +795,11 @@ static int launch_scan(const ChessState& st, const Workspace& ws, const SelParam
                        cudaStream_t stream) {
   using SC = ScanCfg<T>;
   const size_t smem = 128 + (size_t)SC::kStages * SC::kStageBytes + 2 * SC::kStages * 8 +
-                      (size_t)(st.d.batch + 1) * sizeof(int);
+                      (size_t)(2 * kMaxBatch + 1) * sizeof(int);
   static bool configured = false;
   if (!configured) {
     const size_t smem_max = 128 + (size_t)SC::kStages * SC::kStageBytes + 2 * SC::kStages * 8 +
-                            (size_t)(kMaxBatch + 1) * sizeof(int);
+                            (size_t)(2 * kMaxBatch + 1) * sizeof(int);
     cudaFuncSetAttribute(select_scan_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_max);
     configured = true;
   }
@@ -665,7 +807,7 @@ static int launch_scan(const ChessState& st, const Workspace& ws, const SelParam
   return check_launch("select_scan");
 }
 
-// persistent scan: one CTA per SM (128 KB TMA ring each), one launch per level
+// persistent scan: one CTA per SM (192 KB TMA ring each), one launch per level
 int launch_select(const ChessState& st, const Workspace& ws, const SelParams& prm, int /*grid*/,
                   cudaStream_t stream) {
   const int nlev = prm.full_scan ? 1 : 3;
@@ -739,3 +881,11 @@ int launch_build_ws_all(const ChessState& st, cudaStream_t stream) {
 }
 
 }  // namespace chess
+
+extern "C" int chess_debug_select_trace(unsigned long long* host_out) {
+  return cudaMemcpyFromSymbol(host_out, chess::g_sel_trace, sizeof(chess::g_sel_trace)) == cudaSuccess ? 0 : 8;
+}
+
+extern "C" int chess_debug_select_tail_trace(unsigned long long* host_out) {
+  return cudaMemcpyFromSymbol(host_out, chess::g_tail_trace, sizeof(chess::g_tail_trace)) == cudaSuccess ? 0 : 8;
+}
