@@ -47,7 +47,7 @@ struct AttnArgs {
   float* lse;
   float scale_log2;  // softmax_scale * log2(e)
   int layer;
-  int mode;  // debug (CHESS_ATTN_MODE): 0 normal, 1 loads only (no math), 2 math only (no K/V loads), 5 exit at entry, 6 exit after the prologue
+  int mode;  // debug (CHESS_ATTN_MODE): 0 normal, 1 loads only (no math), 2 math only (no K/V loads), 5 exit at entry, 6 exit after the prologue, 7 force stream-K
 };
 
 // Debug timeline (read by chess_debug_attn_trace): per CTA globaltimer stamps
@@ -237,7 +237,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int s = b0 + lane;
       nseg += __popc(__ballot_sync(0xffffffffu, s < nb && s_np[s] > 0)) * H;
     }
-    const int kp = nseg > 0 && nseg <= G0 ? G0 / nseg : 0;  // 0: stream-K mode
+    const int kp = (args.mode != 7 && nseg > 0 && nseg <= G0) ? G0 / nseg : 0;  // 0: stream-K mode
     int prun = 0;
     for (int b0 = 0; b0 < nb; b0 += 32) {
       const int s = b0 + lane;
@@ -328,43 +328,52 @@ __global__ void __launch_bounds__(kThreads, 1)
     };
     int cur_row, cur_tag, nxt_row = 0, nxt_tag = -1;
     fetch(0, cur_row, cur_tag);
-    int stage = 0, qk = 0;
-    uint32_t ph = 0;
+    int qk = 0;
     for (int base = 0; base < n; base += 32) {
       if (base + 32 < n) fetch(base + 32, nxt_row, nxt_tag);
       const int cnt = min(32, n - base);
-      for (int i = 0; i < cnt; ++i) {
-        const int row0 = __shfl_sync(0xffffffffu, cur_row, i);
-        const int tag = __shfl_sync(0xffffffffu, cur_tag, i);
-        if (lane == 0) {
-          if (tag >= 0) {  // first page of a piece: its q rows into the q ring
+      // Pages go out in runs of <= 8 that never cross a piece start; a run
+      // that begins a piece first sends that piece's q rows (q ring order =
+      // page order, so the 2-slot q ring cannot deadlock).  Within a run,
+      // lane 4p+b issues box b of page p: the TMA issues run in parallel.
+      const uint32_t starts = __ballot_sync(0xffffffffu, cur_tag >= 0);
+      for (int c0 = 0; c0 < cnt;) {
+        const uint32_t later = starts & ~((2u << c0) - 1u);  // starts after c0
+        const int nxt_start = later ? __ffs(later) - 1 : 32;
+        const int c1 = min(min(c0 + 8, cnt), nxt_start);
+        if ((starts >> c0) & 1u) {
+          const int tag = __shfl_sync(0xffffffffu, cur_tag, c0);
+          if (lane == 0) {
             if (qk == 0) pdl_wait();
             const int qs = qk & 1;
             mbar_wait(&qempty[qs], (uint32_t)(((qk >> 1) & 1) ^ 1));
             mbar_arrive_expect_tx(&qfull[qs], (uint32_t)C::kQBytes);
             const __nv_bfloat16* qsrc = args.q + (int64_t)(tag >> 8) * args.q_stride + (int64_t)(tag & 255) * GQ * HD;
             tma_load_1d(qbuf + qs * C::kQBytes, qsrc, (uint32_t)C::kQBytes, &qfull[qs]);
-            ++qk;
           }
-          mbar_wait(&empty[stage], ph ^ 1u);
-          if (args.mode == 2) {
-            mbar_arrive(&full[stage]);
-          } else {
-            mbar_arrive_expect_tx(&full[stage], (uint32_t)C::kStageBytes);
-            const uint32_t kdst = smem_u32(ring + (size_t)stage * C::kStageBytes);
-            const uint32_t bar = smem_u32(&full[stage]);
-#pragma unroll
-            for (int cb = 0; cb < C::kCB; ++cb) {
-              tma_load_3d(kdst + cb * (B * 128), &kmap, cb * 64, row0, args.layer, bar);
-              tma_load_3d(kdst + C::kPageBytes + cb * (B * 128), &vmap, cb * 64, row0, args.layer, bar);
-            }
-          }
-          st_release_cta(&ctr[0], base + i + 1);
+          ++qk;
         }
-        if (++stage == C::kStages) {
-          stage = 0;
-          ph ^= 1u;
+        const int pg = lane >> 2, bx = lane & 3;
+        const int i = c0 + pg;
+        const int row0 = __shfl_sync(0xffffffffu, cur_row, min(i, 31));
+        const bool live = i < c1;
+        const int j = base + i;
+        const int stg = j % C::kStages;
+        const uint32_t ph = (uint32_t)((j / C::kStages) & 1);
+        if (live && bx == 0) {
+          mbar_wait(&empty[stg], ph ^ 1u);
+          if (args.mode == 2) mbar_arrive(&full[stg]);
+          else mbar_arrive_expect_tx(&full[stg], (uint32_t)C::kStageBytes);
         }
+        __syncwarp();
+        if (live && args.mode != 2 && bx < 2 * C::kCB) {
+          const uint32_t dst = smem_u32(ring + (size_t)stg * C::kStageBytes) +
+                               (bx / C::kCB) * C::kPageBytes + (bx % C::kCB) * (B * 128);
+          tma_load_3d(dst, bx / C::kCB ? &vmap : &kmap, (bx % C::kCB) * 64, row0, args.layer, smem_u32(&full[stg]));
+        }
+        __syncwarp();
+        if (lane == 0) st_release_cta(&ctr[0], base + c1);
+        c0 = c1;
       }
       cur_row = nxt_row;
       cur_tag = nxt_tag;

@@ -19,6 +19,8 @@
 // them in fixed slice order (deterministic), runs the radix top-k and writes
 // the next level's candidate list, or — at the page level — the semantic set,
 // working set and block table.
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace chess {
@@ -803,7 +805,8 @@ static int launch_scan(const ChessState& st, const Workspace& ws, const SelParam
     cudaFuncSetAttribute(select_scan_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_max);
     configured = true;
   }
-  select_scan_kernel<T><<<num_sms(), kScanCTA, smem, stream>>>(st, ws, prm, level);
+  static const int grid_override = getenv("CHESS_SELECT_GRID") ? atoi(getenv("CHESS_SELECT_GRID")) : 0;  // debug
+  select_scan_kernel<T><<<grid_override > 0 ? grid_override : num_sms(), kScanCTA, smem, stream>>>(st, ws, prm, level);
   return check_launch("select_scan");
 }
 
