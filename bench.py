@@ -91,6 +91,19 @@ class ClockSampler:
                 "samples": len(self.samples)}
 
 
+def _ncu_traffic(cfg_name, kernel):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of `kernel`
+    from the latest committed `ncu --set full` capture of this config
+    (profiles/traffic.json, written from profiles/r*/ncu_*.txt), or None."""
+    f = REPO / "profiles" / "traffic.json"
+    if not f.exists():
+        return None
+    try:
+        return json.loads(f.read_text()).get(cfg_name, {}).get(kernel)
+    except (ValueError, OSError):
+        return None
+
+
 # ---------------------------------------------------------------------------
 # GPU arm
 # ---------------------------------------------------------------------------
@@ -141,11 +154,13 @@ def run_gpu(args):
         torch.cuda.synchronize()
         return dec
 
+    outs = [wl.out, torch.zeros_like(wl.out)]  # double-buffered step outputs (e2e D2H overlap)
+
     def capture_ring(dec):
         graphs = []
         for r in range(ring):
             k, v, q, lg = wl.step_inputs(r)
-            graphs.append(dec.capture(k, v, q, lg, wl.out))
+            graphs.append(dec.capture(k, v, q, lg, outs[r % 2]))
         return graphs
 
     def timed(dec, graphs, steps, warmup, sample_clocks=False):
@@ -215,31 +230,46 @@ def run_gpu(args):
     res = timed(dec, graphs, args.steps, args.warmup, sample_clocks=True)
     results["select_every_step"] = res
 
-    # ---- kernel-level timing (CUDA events on the launching stream) ----
-    stream = torch.cuda.current_stream()
+    # ---- kernel-level timing: the kernels alone, captured in CUDA graphs
+    # (no host gaps) and timed with CUDA events on the replay stream ----
     k, v, q, lg = wl.step_inputs(0)
-    ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
-    reps = 5
+    reps = 3
+    gs = torch.cuda.Stream()
+    gs.wait_stream(torch.cuda.current_stream())
+    g_attn, g_sel = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g_attn, stream=gs):
+        for _ in range(reps):
+            for layer in range(L):
+                dec.attend(layer, q[:, layer], wl.out[:, layer], stream=gs)
+    with torch.cuda.graph(g_sel, stream=gs):
+        for _ in range(reps):
+            dec.select(force_all=True, stream=gs)
+    torch.cuda.current_stream().wait_stream(gs)
+    g_attn.replay()
+    g_sel.replay()
     torch.cuda.synchronize()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+    stream = torch.cuda.current_stream()
     ev[0].record(stream)
-    for _ in range(reps):
-        for layer in range(L):
-            dec.attend(layer, q[:, layer], wl.out[:, layer])
+    g_attn.replay()
     ev[1].record(stream)
-    for _ in range(reps):
-        dec.select(force_all=True)
+    g_sel.replay()
     ev[2].record(stream)
     torch.cuda.synchronize()
     attn_launch_s = ev[0].elapsed_time(ev[1]) / 1e3 / (reps * L)
     select_call_s = ev[1].elapsed_time(ev[2]) / 1e3 / reps
+    del g_attn, g_sel
     ws_now = st.ws_len.float().mean().item()
     fill_now = float(st.tail_fill.float().mean().item())
     attn_launch_bytes = attn_bytes_per_layer(ws_now, fill_now)
     sel_call_bytes = select_bytes(st.sel_stats.cpu().numpy())
 
-    # ---- e2e through the C-ABI with host buffers (pinned), headline variant ----
+    # ---- e2e through the public step API with host buffers (pinned),
+    # headline variant.  Every step's inputs are copied host->device and its
+    # attention output device->host inside the timed region; the copies run
+    # on their own streams, pipelined one step ahead/behind the compute. ----
     hk = [t.cpu().pin_memory() for t in (wl.k_ring[0], wl.v_ring[0], wl.q_ring[0], wl.logit_ring[0])]
-    h_out = torch.empty(wl.out.shape, dtype=wl.out.dtype).pin_memory()
+    h_out = [torch.empty(wl.out.shape, dtype=wl.out.dtype).pin_memory() for _ in range(2)]
     dec = fresh_decoder("every_step")
     graphs = capture_ring(dec)
     for t in range(args.warmup):
@@ -247,17 +277,41 @@ def run_gpu(args):
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
+    comp = torch.cuda.current_stream()
+    cs, ds = torch.cuda.Stream(), torch.cuda.Stream()
+    h2d_ev = [torch.cuda.Event() for _ in range(ring)]
+    out_ev = [torch.cuda.Event() for _ in range(2)]
+    d2h_ev = [torch.cuda.Event() for _ in range(2)]
+
+    def h2d(r):
+        with torch.cuda.stream(cs):
+            wl.k_ring[r].copy_(hk[0], non_blocking=True)
+            wl.v_ring[r].copy_(hk[1], non_blocking=True)
+            wl.q_ring[r].copy_(hk[2], non_blocking=True)
+            wl.logit_ring[r].copy_(hk[3], non_blocking=True)
+            h2d_ev[r].record(cs)
+
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
+    e0.record(comp)
+    cs.wait_stream(comp)
+    ds.wait_stream(comp)
+    h2d((args.warmup) % ring)
     for t in range(args.steps):
         r = (args.warmup + t) % ring
-        wl.k_ring[r].copy_(hk[0], non_blocking=True)
-        wl.v_ring[r].copy_(hk[1], non_blocking=True)
-        wl.q_ring[r].copy_(hk[2], non_blocking=True)
-        wl.logit_ring[r].copy_(hk[3], non_blocking=True)
+        if t + 1 < args.steps:
+            h2d((args.warmup + t + 1) % ring)
+        comp.wait_event(h2d_ev[r])
+        if t >= 2:
+            comp.wait_event(d2h_ev[t % 2])  # out buffer t%2 drained to host
         graphs[r].replay()
-        h_out.copy_(wl.out, non_blocking=True)
-    e1.record()
+        out_ev[t % 2].record(comp)
+        with torch.cuda.stream(ds):
+            ds.wait_event(out_ev[t % 2])
+            h_out[t % 2].copy_(outs[r % 2], non_blocking=True)
+            d2h_ev[t % 2].record(ds)
+    comp.wait_stream(ds)
+    comp.wait_stream(cs)
+    e1.record(comp)
     torch.cuda.synchronize()
     e2e_ms = e0.elapsed_time(e1)
     if world > 1:
@@ -265,7 +319,7 @@ def run_gpu(args):
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         e2e_ms = tt.item()
     h2d = sum(t.numel() * t.element_size() for t in hk)
-    d2h = h_out.numel() * h_out.element_size()
+    d2h = h_out[0].numel() * h_out[0].element_size()
 
     # ---- amortised dynamic (backtracking) and attention-only variants ----
     if not args.headline_only:
@@ -321,7 +375,7 @@ def run_gpu(args):
             "peak_source": peak_src,
             "unit": "GB/s",
             "frac": achieved / hbm_peak,
-            "traffic": None,
+            "traffic": _ncu_traffic(cfg_name, "sparse_decode"),
             "bytes_per_launch": attn_launch_bytes,
             "launch_us": attn_launch_s * 1e6,
         },
