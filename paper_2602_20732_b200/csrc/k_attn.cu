@@ -8,20 +8,22 @@
 //
 // B200 design — HBM-bound, one persistent CTA per SM:
 //  * work list = every (slot, kv head, working-set page) of the layer, laid
-//    out segment by segment (segment = one (slot, kv head)); CTA c owns the
-//    contiguous page range [c*N/G, (c+1)*N/G) (stream-K at page granularity,
-//    so every CTA streams the same bytes +-1 page);
-//  * warp 8 is the TMA producer: it reads the block-table entries of 32
-//    upcoming pages with one coalesced load (prefetched one batch ahead), then
-//    lane 0 issues 2-D tensor loads (128B swizzle, [64 cols x B rows] boxes)
-//    of each page's K and V into an S-stage shared-memory ring — no dependent
-//    global load sits between two TMA issues;
-//  * warps 0-7 consume pages round-robin (page j -> warp j % 8): QK^T and PV
-//    on the tensor cores with mma.sync m16n8k16 (bf16 in, fp32 accumulate;
-//    the GQA group's q heads are the M rows), online softmax in registers;
-//  * at the end of each segment piece the 8 warp states are merged in smem in
-//    warp order; a segment split across CTAs is merged by the last CTA to
-//    finish it (atomic counter), in CTA order — deterministic.
+//    out segment by segment (segment = one (slot, kv head)).  Piece mode
+//    (segments <= CTAs): each segment is cut into k = floor(G/segments)
+//    pieces of >= 4 pages, one per CTA (no merge when k = 1).  Stream-K
+//    (more segments): CTA c owns pages [c*N/G, (c+1)*N/G);
+//  * the last warp is the TMA producer: block-table ids of 32 pages come from
+//    one coalesced load (prefetched a batch ahead); pages go out in runs whose
+//    2-D tensor loads (128B swizzle, [64 cols x B rows] boxes) are issued by
+//    4 lanes per page in parallel into an S-stage ring of K+V page tiles; each
+//    piece's GQA q rows go through a 2-slot q ring; the first run is issued
+//    before griddepcontrol.wait so it overlaps the previous kernel;
+//  * consumer warps take pages round-robin: S^T = K q^T and O^T += V^T P^T
+//    with mma.sync m16n8k16 (tokens as M; P^T via movmatrix, never in smem),
+//    online softmax per head in registers;
+//  * piece states are merged asynchronously by the last consumer warp to
+//    arrive (warp order); a split segment is merged by the last CTA to finish
+//    it (atomic counter), in CTA order — deterministic.
 #include <cudaTypedefs.h>
 
 #include <cstdlib>
@@ -32,12 +34,24 @@ namespace chess {
 
 namespace {
 
-constexpr int kConsumers = 8;
+// Consumer warps per CTA and CTAs per SM (build-time knobs).  Measured on
+// B200, cfg3 layer (tools/attn_micro.py, graph-replayed): 4 consumers x 1 CTA
+// (13-stage ring) 19.1 us; 8 x 1: 19.8 us; 6 x 2: 28.1 us; 8 x 2: 34.4 us --
+// two co-resident CTAs halve each ring and the layers fight for HBM.
+#ifndef CHESS_ATTN_CONSUMERS
+#define CHESS_ATTN_CONSUMERS 4
+#endif
+#ifndef CHESS_ATTN_CTAS_PER_SM
+#define CHESS_ATTN_CTAS_PER_SM 1
+#endif
+constexpr int kConsumers = CHESS_ATTN_CONSUMERS;
+constexpr int kCtasPerSm = CHESS_ATTN_CTAS_PER_SM;
+constexpr int kAttnMaxBatch = 256;  // per-slot tables live in smem
 constexpr int kMinPiece = 4;  // piece mode: pages per piece >= 4 (bounds the merge fan-in)
 constexpr int kThreads = (kConsumers + 1) * 32;
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kLn2 = 0.6931471805599453f;
-constexpr int kSmemBudget = 227 * 1024 - 256;  // minus static smem
+constexpr int kSmemBudget = (228 * 1024) / kCtasPerSm - 1024 - 256;  // minus reserved + static smem
 
 struct AttnArgs {
   const __nv_bfloat16* q;
@@ -67,7 +81,7 @@ struct Cfg {
   static constexpr int kStateBytes = kConsumers * GQ * kRow * 4;
   static constexpr int kQBytes = GQ * HD * 2;          // one GQA group's q rows (bf16)
   static constexpr int kQSlots = 2;
-  static constexpr int kTables = (kMaxBatch + 1) * 4 * 4;
+  static constexpr int kTables = (kAttnMaxBatch + 1) * 4 * 4;
   static constexpr int kMisc = kTables + 64 * 8 + 64 + 1024;  // tables, barriers, counters, align
   static constexpr int kStagesRaw = (kSmemBudget - kStateBytes - kQSlots * kQBytes - kMisc) / kStageBytes;
   static constexpr int kStages = kStagesRaw > 32 ? 32 : kStagesRaw;
@@ -168,7 +182,7 @@ __device__ __forceinline__ void st_release_cta(int* p, int v) {
 //    in warp order and writes the output, or the split-segment partial and the
 //    cross-CTA combine.  The slot is reopened via `st_next`.
 template <int HD, int GQ, int B>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kThreads, kCtasPerSm)
     sparse_decode_kernel(ChessState st, Workspace ws, AttnArgs args,
                          const __grid_constant__ CUtensorMap kmap,
                          const __grid_constant__ CUtensorMap vmap) {
@@ -184,9 +198,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* qempty = qfull + C::kQSlots;
   int* ctr = reinterpret_cast<int*>(qempty + C::kQSlots);  // [0] issued, [1] st_cnt, [2] st_next
   int* prefix = ctr + 16;                                   // [nb + 1] pages before slot s
-  int* s_np = prefix + kMaxBatch + 1;                       // [nb] pages per segment of slot s
-  int* s_fill = s_np + kMaxBatch;                            // [nb] valid rows of the last page
-  int* ppre = s_fill + kMaxBatch;                            // [nb + 1] pieces before slot s (piece mode)
+  int* s_np = prefix + kAttnMaxBatch + 1;                   // [nb] pages per segment of slot s
+  int* s_fill = s_np + kAttnMaxBatch;                        // [nb] valid rows of the last page
+  int* ppre = s_fill + kAttnMaxBatch;                        // [nb + 1] pieces before slot s (piece mode)
   const ChessDims& d = st.d;
   const int H = d.kv_heads;
   const int nb = d.batch;
@@ -337,12 +351,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       // page order, so the 2-slot q ring cannot deadlock).  Within a run,
       // lane 4p+b issues box b of page p: the TMA issues run in parallel.
       const uint32_t starts = __ballot_sync(0xffffffffu, cur_tag >= 0);
+      constexpr int kRun = C::kStages < 8 ? C::kStages : 8;  // distinct stages within a run
       for (int c0 = 0; c0 < cnt;) {
         const uint32_t later = starts & ~((2u << c0) - 1u);  // starts after c0
         const int nxt_start = later ? __ffs(later) - 1 : 32;
-        const int c1 = min(min(c0 + 8, cnt), nxt_start);
-        if ((starts >> c0) & 1u) {
-          const int tag = __shfl_sync(0xffffffffu, cur_tag, c0);
+        const int c1 = min(min(c0 + kRun, cnt), nxt_start);
+        const bool first_run = qk == 0 && base == 0 && c0 == 0;
+        auto issue_q = [&](int at) {
+          const int tag = __shfl_sync(0xffffffffu, cur_tag, at);
           if (lane == 0) {
             if (qk == 0) pdl_wait();
             const int qs = qk & 1;
@@ -352,7 +368,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             tma_load_1d(qbuf + qs * C::kQBytes, qsrc, (uint32_t)C::kQBytes, &qfull[qs]);
           }
           ++qk;
-        }
+        };
+        // the kernel's first q load waits for the previous grid (PDL); the
+        // first run of K/V pages is issued before it so it overlaps that wait
+        if (((starts >> c0) & 1u) && !first_run) issue_q(c0);
         const int pg = lane >> 2, bx = lane & 3;
         const int i = c0 + pg;
         const int row0 = __shfl_sync(0xffffffffu, cur_row, min(i, 31));
@@ -373,6 +392,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         __syncwarp();
         if (lane == 0) st_release_cta(&ctr[0], base + c1);
+        if (first_run) issue_q(0);
         c0 = c1;
       }
       cur_row = nxt_row;
@@ -773,8 +793,8 @@ int launch_sparse_decode(const ChessState& st, const Workspace& ws, int layer, c
   const int nctas = ws.attn_ctas;
   if ((reinterpret_cast<uintptr_t>(q) & 15) || (q_stride & 7))
     return fail(CHESS_ERR_UNSUPPORTED, "sparse_decode: q must be 16-byte aligned with q_stride %% 8 == 0");
-  if (d.kv_heads > 255 || d.batch > (1 << 22))
-    return fail(CHESS_ERR_UNSUPPORTED, "sparse_decode: kv_heads must be <= 255");
+  if (d.kv_heads > 255 || d.batch > kAttnMaxBatch)
+    return fail(CHESS_ERR_UNSUPPORTED, "sparse_decode: kv_heads must be <= 255 and batch <= %d", kAttnMaxBatch);
 #define CHESS_ATTN_CASE(HD_, GQ_, B_)                                        \
   if (d.head_dim == HD_ && gq == GQ_ && d.page_size == B_)                   \
     return launch_inst<HD_, GQ_, B_>(st, ws, a, nctas, stream);
