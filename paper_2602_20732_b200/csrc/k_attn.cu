@@ -123,6 +123,15 @@ __device__ __forceinline__ uint32_t movm_t(uint32_t x) {
   return y;
 }
 
+__device__ __forceinline__ void tma_load_4d(uint32_t dst, const CUtensorMap* map, int c0, int c1,
+                                            int c2, int c3, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
+      "%3, %4, %5}], [%6];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(bar)
+      : "memory");
+}
+
 __device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map, int c0, int c1,
                                             int c2, uint32_t bar) {
   asm volatile(
@@ -385,10 +394,9 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
           else mbar_arrive_expect_tx(&full[stg], (uint32_t)C::kStageBytes);
         }
         __syncwarp();
-        if (live && args.mode != 2 && bx < 2 * C::kCB) {
-          const uint32_t dst = smem_u32(ring + (size_t)stg * C::kStageBytes) +
-                               (bx / C::kCB) * C::kPageBytes + (bx % C::kCB) * (B * 128);
-          tma_load_3d(dst, bx / C::kCB ? &vmap : &kmap, (bx % C::kCB) * 64, row0, args.layer, smem_u32(&full[stg]));
+        if (live && args.mode != 2 && bx < 2) {  // lane 4p: K tile, 4p+1: V tile
+          const uint32_t dst = smem_u32(ring + (size_t)stg * C::kStageBytes) + bx * C::kPageBytes;
+          tma_load_4d(dst, bx ? &vmap : &kmap, 0, row0, 0, args.layer, smem_u32(&full[stg]));
         }
         __syncwarp();
         if (lane == 0) st_release_cta(&ctr[0], base + c1);
@@ -722,15 +730,19 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 
 // 3-D view [layers][n_phys*kv_heads*page][head_dim] of a KV pool; boxes of
 // 64 columns x one page of rows with 128-byte swizzle.
+// 4-D view of a KV pool: (64 columns, pool rows, HD/64 column blocks,
+// layers) with strides (2 B, HD*2 B, 128 B, pool bytes).  One box
+// (64, B, HD/64, 1) is a whole (page, head) K or V tile, landing in smem as
+// [column block][B rows][128 B] with 128B swizzle — one TMA op per tile.
 int make_kv_map(CUtensorMap* m, const void* base, const ChessDims& d) {
   auto fn = encode_fn();
   if (!fn) return fail(CHESS_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
   const cuuint64_t rows = (cuuint64_t)d.n_phys * d.kv_heads * d.page_size;
-  cuuint64_t dims[3] = {(cuuint64_t)d.head_dim, rows, (cuuint64_t)d.layers};
-  cuuint64_t strides[2] = {(cuuint64_t)d.head_dim * 2, rows * d.head_dim * 2};
-  cuuint32_t box[3] = {64, (cuuint32_t)d.page_size, 1};
-  cuuint32_t es[3] = {1, 1, 1};
-  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box,
+  cuuint64_t dims[4] = {64, rows, (cuuint64_t)d.head_dim / 64, (cuuint64_t)d.layers};
+  cuuint64_t strides[3] = {(cuuint64_t)d.head_dim * 2, 128, rows * d.head_dim * 2};
+  cuuint32_t box[4] = {64, (cuuint32_t)d.page_size, (cuuint32_t)d.head_dim / 64, 1};
+  cuuint32_t es[4] = {1, 1, 1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides, box,
                   es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(CHESS_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
