@@ -127,18 +127,32 @@ def run_gpu(args):
     cfg_name = args.config
     c = CONFIGS[cfg_name]
     batch = c["batch"] if args.batch is None else args.batch
-    # cfg4 is batch-sharded: total batch split across ranks; others replicate per rank
-    if cfg_name == "cfg4" and args.batch is None:
+    # sharding: cfg4 splits its batch across ranks, cfg5 its KV
+    # heads; other configs run one replica per rank (weak scaling)
+    shard = args.shard
+    if shard == "auto":
+        shard = {"cfg4": "batch", "cfg5": "head"}.get(cfg_name, "replica") if world > 1 else "replica"
+    if shard == "batch" and args.batch is None:
         batch = max(1, c["batch"] // world)
+    head = shard == "head"
     total_steps = args.warmup + args.steps
     ring = 64 if c["page"] == 32 else 32
     gen_pages = math.ceil((total_steps + 2 * ring + 64) / c["page"]) + 4
     wl = SyntheticDecode(cfg_name, batch=batch, gen_pages=gen_pages, ring=ring, seed=rank,
-                         summary_dtype=args.summary_dtype)
+                         summary_dtype=args.summary_dtype, head_shard=(rank, world) if head else None)
     st = wl.st
     sh = wl.shape
     sel = preset_config("aggressive", page_size=sh.page_size)
     P, B, L = wl.P, wl.B, sh.layers
+    exchange = None
+    if head:
+        from paper_2602_20732_b200.parallel import HeadShard, HeadShardExchange
+
+        hs = HeadShard(rank, world, L, c["kv_heads"], c["q_heads"], c["head_dim"])
+        exchange = HeadShardExchange(hs, batch, sh.max_pages, sh.pages_per_chunk, sh.chunks_per_grid,
+                                     torch.device("cuda", local), full_scan=args.full_scan)
+    # sequences the whole job advances per step
+    job_batch = batch if head else world * batch
 
     def fresh_decoder(policy, thresholds=None):
         st.reset()
@@ -146,15 +160,23 @@ def run_gpu(args):
         st.tail_fill.fill_(B)
         st.token_count.fill_(P * B)
         st.sink_count.fill_(1)
-        dec = ChessDecoder(st, sel, policy=policy, thresholds=thresholds, full_scan=args.full_scan)
+        dec = ChessDecoder(st, sel, policy=policy, thresholds=thresholds, full_scan=args.full_scan,
+                           exchange=exchange)
         wl.prefill(dec)
-        # one eager step: first-call attribute/occupancy setup happens outside capture
+        # one eager step: first-call attribute/occupancy setup (and the NCCL
+        # communicator) happen outside capture
         k, v, q, lg = wl.step_inputs(ring - 1)
-        dec.step(k, v, q, lg, wl.out)
+        dec.step(k, v, q, lg, outs[0])
         torch.cuda.synchronize()
         return dec
 
-    outs = [wl.out, torch.zeros_like(wl.out)]  # double-buffered step outputs (e2e D2H overlap)
+    # double-buffered step outputs (e2e D2H overlap); head shard: per-layer
+    # gather buffers [L, world, b, H_q/n, d]
+    if head:
+        outs = [torch.zeros((L, world, batch, sh.q_heads, sh.head_dim), dtype=torch.bfloat16,
+                            device=wl.out.device) for _ in range(2)]
+    else:
+        outs = [wl.out, torch.zeros_like(wl.out)]
 
     def capture_ring(dec):
         graphs = []
@@ -269,7 +291,7 @@ def run_gpu(args):
     # attention output device->host inside the timed region; the copies run
     # on their own streams, pipelined one step ahead/behind the compute. ----
     hk = [t.cpu().pin_memory() for t in (wl.k_ring[0], wl.v_ring[0], wl.q_ring[0], wl.logit_ring[0])]
-    h_out = [torch.empty(wl.out.shape, dtype=wl.out.dtype).pin_memory() for _ in range(2)]
+    h_out = [torch.empty(outs[0].shape, dtype=outs[0].dtype).pin_memory() for _ in range(2)]
     dec = fresh_decoder("every_step")
     graphs = capture_ring(dec)
     for t in range(args.warmup):
@@ -333,7 +355,7 @@ def run_gpu(args):
 
     head = results["select_every_step"]
     ms_step = head["ms"] / args.steps
-    value = world * batch / (ms_step / 1e3)
+    value = job_batch / (ms_step / 1e3)
     bytes_step = step_bytes(head, True)
     achieved = attn_launch_bytes / attn_launch_s / 1e9
     out = {
@@ -346,7 +368,7 @@ def run_gpu(args):
         "ms_per_step": ms_step,
         "us_per_step": ms_step * 1e3,
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": "strong" if head else "weak",
         "vs_baseline": None,
         "dtype": "bf16 KV / f32 summaries / f64 scores",
         "data": "synthetic (planted-relevance keys, random-init shapes)",
@@ -356,7 +378,12 @@ def run_gpu(args):
             "context": c["ctx"],
             "page_size": B,
             "preset": "aggressive (0.5, 0.2, 0.1), W=4, sinks=1",
-            "parallelism": f"batch-shard x{world}" if world > 1 else "single GPU",
+            "parallelism": ("single GPU" if world == 1 and shard == "replica" else
+                            {"batch": f"batch-shard x{world} (no data-path collective)",
+                             "head": f"kv-head-shard x{world} (NCCL: per-level partial-score "
+                                     f"all-gather + per-layer output all-gather)",
+                             "replica": f"replicas x{world} (no data-path collective)"}[shard]),
+            "batch_total": job_batch,
             "summary_dtype": args.summary_dtype,
             "scan": "full (Alg.1 literal)" if args.full_scan else "conditional (output-identical)",
             "kv_pool_pages": sh.n_phys,
@@ -387,18 +414,18 @@ def run_gpu(args):
             "bytes_per_call": sel_call_bytes, "call_us": select_call_s * 1e6,
         },
         "e2e": {
-            "value": world * batch * args.steps / (e2e_ms / 1e3),
+            "value": job_batch * args.steps / (e2e_ms / 1e3),
             "unit": "tokens/s",
             "h2d_bytes_per_step": h2d,
             "d2h_bytes_per_step": d2h,
         },
-        "gpu_launches": args.steps * (L + 6),
+        "gpu_launches": args.steps * (L + 6 + (3 if head else 0)),  # + select_combine per level
         "clocks": head["clocks"],
     }
     if not args.headline_only:
         out["variants"] = {
             name: {"us_per_step": r["ms"] / args.steps * 1e3,
-                   "tokens_per_s": world * batch / (r["ms"] / args.steps / 1e3),
+                   "tokens_per_s": job_batch / (r["ms"] / args.steps / 1e3),
                    "ws_pages_mean": r["ws_mean"]}
             for name, r in results.items()
         }
@@ -507,6 +534,8 @@ def main():
     ap.add_argument("--full-scan", action="store_true")
     ap.add_argument("--headline-only", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--shard", default="auto", choices=["auto", "batch", "head", "replica"],
+                    help="multi-GPU partitioning (auto: cfg4 batch, cfg5 kv-head, else replicas)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -215,6 +215,26 @@ int chess_summary_fold(const ChessState* st, int32_t seq, const void* rows, int3
  * with fire[s] != 0 (or all slots if cfg->force_all). */
 int chess_select(const ChessState* st, const ChessSelectCfg* cfg, void* stream);
 
+/* KV-head-sharded selection (score_all's GEMV is a sum over the
+ * (layer, head) column slices, selection.py:62-74).  Rank r holds kv heads
+ * [r*H/n, (r+1)*H/n) of every layer, so its state's summary rows give
+ * PARTIAL Eq.4 scores.  One cascade level = partial -> caller's all-gather
+ * (NCCL) of `partial` -> combine.  Levels 0, 1, 2 (grids, chunks of kept
+ * grids, pages of kept chunks) for the conditional scan; level 3 alone for
+ * cfg->full_scan.
+ *   partial  : f64 [batch][ld_partial]  this rank's partial scores, in the
+ *              level's candidate order (written for slots that fired)
+ *   gathered : f64 [world][batch][ld_partial]  every rank's `partial`,
+ *              rank-major; summed in rank order, so all ranks select
+ *              identically
+ * ld_partial >= the level's row capacity (max_grids, max_chunks, max_pages,
+ * or their sum for level 3).  Combine at level 2 (or 3) writes the semantic
+ * set, working set and block table exactly as chess_select. */
+int chess_select_partial(const ChessState* st, const ChessSelectCfg* cfg, int32_t level,
+                         double* partial, int64_t ld_partial, void* stream);
+int chess_select_combine(const ChessState* st, const ChessSelectCfg* cfg, int32_t level,
+                         const double* gathered, int32_t world, int64_t ld_partial, void* stream);
+
 /* K3 epilogue alone: rebuild working set + block table from the cached
  * semantic set for all slots (selection.py:126-140). */
 int chess_build_working_set(const ChessState* st, void* stream);

@@ -112,6 +112,8 @@ SIGNATURES = {
     "chess_summary_from_vectors": (C.c_int, [C.POINTER(ChessState), _I32, _P, _I32, _I64, _P]),
     "chess_summary_fold": (C.c_int, [C.POINTER(ChessState), _I32, _P, _I32, _I32, _I64, _P]),
     "chess_select": (C.c_int, [C.POINTER(ChessState), C.POINTER(ChessSelectCfg), _P]),
+    "chess_select_partial": (C.c_int, [C.POINTER(ChessState), C.POINTER(ChessSelectCfg), _I32, _P, _I64, _P]),
+    "chess_select_combine": (C.c_int, [C.POINTER(ChessState), C.POINTER(ChessSelectCfg), _I32, _P, _I32, _I64, _P]),
     "chess_build_working_set": (C.c_int, [C.POINTER(ChessState), _P]),
     "chess_sparse_decode": (C.c_int, [C.POINTER(ChessState), _I32, _P, _I64, _P, _I64, _P, _F, _P]),
     "chess_entropy_trigger": (C.c_int, [C.POINTER(ChessState), _P, _I64, _I64, C.POINTER(ChessTriggerCfg), _P, _P]),

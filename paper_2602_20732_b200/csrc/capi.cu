@@ -20,6 +20,9 @@ int launch_from_vectors(const ChessState&, int, const double*, int, int64_t, con
                         cudaStream_t);
 int launch_mean_rows(const void*, int, int64_t, int64_t, int64_t, double*, cudaStream_t);
 int launch_select(const ChessState&, const Workspace&, const SelParams&, int, cudaStream_t);
+int launch_select_partial(const ChessState&, const Workspace&, const SelParams&, int, cudaStream_t);
+int launch_select_combine(const ChessState&, const Workspace&, const SelParams&, int,
+                          const double*, int, cudaStream_t);
 int launch_build_ws_all(const ChessState&, cudaStream_t);
 int launch_score_rows(const void*, int, int64_t, int64_t, int64_t, const double*, double*,
                       cudaStream_t);
@@ -260,15 +263,12 @@ int chess_record_entropy(const ChessState* st, const double* entropy, const uint
   return launch_record_entropy(*st, entropy, active, *cfg, (cudaStream_t)stream);
 }
 
-int chess_select(const ChessState* st, const ChessSelectCfg* cfg, void* stream) {
-  Workspace ws;
-  int rc = state_ws(st, &ws);
-  if (rc) return rc;
+static int select_params(const ChessSelectCfg* cfg, SelParams* out) {
   if (!cfg) return fail(CHESS_ERR_CONFIG, "null select cfg");
   const double r[3] = {cfg->rho_grid, cfg->rho_chunk, cfg->rho_page};
   for (int i = 0; i < 3; ++i)
     if (!(r[i] > 0.0 && r[i] <= 1.0)) return fail(CHESS_ERR_CONFIG, "ratios must be in (0, 1]");
-  SelParams prm;
+  SelParams prm = {};
   prm.rho[0] = r[0];
   prm.rho[1] = r[1];
   prm.rho[2] = r[2];
@@ -276,8 +276,60 @@ int chess_select(const ChessState* st, const ChessSelectCfg* cfg, void* stream) 
   static const int dbg_mode = getenv("CHESS_SELECT_MODE") ? atoi(getenv("CHESS_SELECT_MODE")) : 0;
   prm.mode = dbg_mode;
   prm.force_all = cfg->force_all;
-  const int grid = 4 * num_sms();
-  return launch_select(*st, ws, prm, grid, (cudaStream_t)stream);
+  *out = prm;
+  return CHESS_OK;
+}
+
+int chess_select(const ChessState* st, const ChessSelectCfg* cfg, void* stream) {
+  Workspace ws;
+  int rc = state_ws(st, &ws);
+  if (rc) return rc;
+  SelParams prm;
+  if ((rc = select_params(cfg, &prm))) return rc;
+  return launch_select(*st, ws, prm, 0, (cudaStream_t)stream);
+}
+
+// rows a level can have for one slot: its exchange row stride must hold them
+static int64_t level_capacity(const ChessDims& d, int level) {
+  const int64_t mc = (d.max_pages + d.pages_per_chunk - 1) / d.pages_per_chunk;
+  const int64_t mg = (mc + d.chunks_per_grid - 1) / d.chunks_per_grid;
+  return level == 0 ? mg : level == 1 ? mc : level == 2 ? (int64_t)d.max_pages : mg + mc + d.max_pages;
+}
+
+static int check_level(const ChessState* st, const ChessSelectCfg* cfg, int32_t level, int64_t ld) {
+  if (cfg->full_scan ? level != 3 : (level < 0 || level > 2))
+    return fail(CHESS_ERR_VALUE, "select level %d invalid (conditional scan: 0..2, full scan: 3)", level);
+  if (ld < level_capacity(st->d, level))
+    return fail(CHESS_ERR_SHAPE, "exchange stride %lld < level %d capacity %lld", (long long)ld, level,
+                (long long)level_capacity(st->d, level));
+  return CHESS_OK;
+}
+
+int chess_select_partial(const ChessState* st, const ChessSelectCfg* cfg, int32_t level,
+                         double* partial, int64_t ld_partial, void* stream) {
+  Workspace ws;
+  int rc = state_ws(st, &ws);
+  if (rc) return rc;
+  SelParams prm;
+  if ((rc = select_params(cfg, &prm))) return rc;
+  if ((rc = check_level(st, cfg, level, ld_partial))) return rc;
+  if (!partial) return fail(CHESS_ERR_SHAPE, "select_partial: null partial buffer");
+  prm.xout = partial;
+  prm.xld = ld_partial;
+  return launch_select_partial(*st, ws, prm, level, (cudaStream_t)stream);
+}
+
+int chess_select_combine(const ChessState* st, const ChessSelectCfg* cfg, int32_t level,
+                         const double* gathered, int32_t world, int64_t ld_partial, void* stream) {
+  Workspace ws;
+  int rc = state_ws(st, &ws);
+  if (rc) return rc;
+  SelParams prm;
+  if ((rc = select_params(cfg, &prm))) return rc;
+  if ((rc = check_level(st, cfg, level, ld_partial))) return rc;
+  if (!gathered || world < 1) return fail(CHESS_ERR_SHAPE, "select_combine: bad gathered buffer / world");
+  prm.xld = ld_partial;
+  return launch_select_combine(*st, ws, prm, level, gathered, world, (cudaStream_t)stream);
 }
 
 int chess_build_working_set(const ChessState* st, void* stream) {

@@ -77,6 +77,11 @@ struct SelParams {
   int32_t full_scan;
   int32_t force_all;
   int32_t mode;  // debug (CHESS_SELECT_MODE): 0 normal, 1 no math, 2 no loads
+  // KV-head shard: when set, the level's tail stops after the
+  // fixed-order slice reduction and exports this rank's PARTIAL scores to
+  // xout[slot * xld + candidate]; select_combine_kernel finishes the level.
+  double* xout;
+  int64_t xld;
 };
 
 // ---------------------------------------------------------------------------

@@ -134,21 +134,17 @@ __device__ void expand_children(const int* parents, int m, int fan, int total_ch
   if (threadIdx.x == 0) *out_n = count;
 }
 
+__device__ void select_tail_topk(const ChessState& st, const Workspace& ws, const SelParams& prm,
+                                 int s, int level, int n, TailSmem& sm);
+
+// Tail of one slot's level: fixed-order slice reduction of the partials into
+// ws.scores[s] (or, head-shard exchange mode, into prm.xout), then the top-k.
 __device__ void select_tail(const ChessState& st, const Workspace& ws, const SelParams& prm, int s,
                             int level, int n, TailSmem& sm) {
-  const ChessDims& d = st.d;
-  const int64_t mr = max_rows(d);
+  const int64_t mr = max_rows(st.d);
   const int ns = ws.n_slices;
   double* sc = ws.scores + (int64_t)s * mr;
-  // keys / kept flags of every level pass fit in smem unless the full-scan
-  // candidate count is large
-  const bool in_smem = n <= kTailCap;  // n bounds every level's candidate count
-  uint64_t* keys = in_smem ? sm.keys : ws.keys + (int64_t)s * mr;
-  int* kept = in_smem ? sm.kept : ws.kept + (int64_t)s * mr;
-  int* plist = ws.plist + (int64_t)s * mr;
   const double* part = ws.part + (int64_t)s * mr * ns;
-  const LevelShape sh = shape_of(st, s);
-  int* stats = st.sel_stats + 8 * s;
 
   // fixed-order reduction over slices (deterministic); the slice partials of
   // a row are loaded together (one round trip) when ns <= 16
@@ -167,10 +163,33 @@ __device__ void select_tail(const ChessState& st, const Workspace& ws, const Sel
       acc = __ldcg(pr);
       for (int q = 1; q < ns; ++q) acc = __dadd_rn(acc, __ldcg(pr + q));
     }
-    sc[i] = acc;
+    if (prm.xout)
+      prm.xout[(int64_t)s * prm.xld + i] = acc;
+    else
+      sc[i] = acc;
   }
   block_sync<kNT>();
   tail_trace(level, s, 2);
+  if (prm.xout) return;  // head shard: exchange, then select_combine_kernel finishes the level
+  select_tail_topk(st, ws, prm, s, level, n, sm);
+}
+
+// Top-k cascade of one tail from the reduced scores ws.scores[s] (candidate
+// order of `level`): keys, ceil-in-double k, radix top-k, then next-level
+// candidates or — at the page level — semantic set + working set.
+__device__ void select_tail_topk(const ChessState& st, const Workspace& ws, const SelParams& prm,
+                                 int s, int level, int n, TailSmem& sm) {
+  const ChessDims& d = st.d;
+  const int64_t mr = max_rows(d);
+  double* sc = ws.scores + (int64_t)s * mr;
+  // keys / kept flags of every level pass fit in smem unless the full-scan
+  // candidate count is large
+  const bool in_smem = n <= kTailCap;  // n bounds every level's candidate count
+  uint64_t* keys = in_smem ? sm.keys : ws.keys + (int64_t)s * mr;
+  int* kept = in_smem ? sm.kept : ws.kept + (int64_t)s * mr;
+  int* plist = ws.plist + (int64_t)s * mr;
+  const LevelShape sh = shape_of(st, s);
+  int* stats = st.sel_stats + 8 * s;
 
   // level order to run in this tail
   const int lv_begin = level == 3 ? 0 : level;
@@ -608,6 +627,33 @@ __global__ void __launch_bounds__(kScanCTA, 1) select_scan_kernel(ChessState st,
 }
 
 // ---------------------------------------------------------------------------
+// KV-head shard: finish one level from every rank's exported
+// partial scores.  gathered = [world][batch][xld] (rank-major, the layout of
+// an all-gather of each rank's xout); the partials are added in rank order so
+// every rank holds bit-identical scores and takes the identical top-k.  One
+// CTA per slot; slots that did not fire (or have no candidates) exit.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kNT) select_combine_kernel(ChessState st, Workspace ws,
+                                                             SelParams prm, int level,
+                                                             const double* gathered, int world) {
+  __shared__ TailSmem sm;
+  const int s = blockIdx.x;
+  const int n = level_rows(st, ws, prm, s, level);
+  if (n == 0) return;
+  const int64_t mr = max_rows(st.d);
+  const int64_t rstride = (int64_t)st.d.batch * prm.xld;
+  const double* g = gathered + (int64_t)s * prm.xld;
+  double* sc = ws.scores + (int64_t)s * mr;
+  for (int i = threadIdx.x; i < n; i += kNT) {
+    double acc = __ldcg(g + i);
+    for (int r = 1; r < world; ++r) acc = __dadd_rn(acc, __ldcg(g + r * rstride + i));
+    sc[i] = acc;
+  }
+  block_sync<kNT>();
+  select_tail_topk(st, ws, prm, s, level, n, sm);
+}
+
+// ---------------------------------------------------------------------------
 // generic function-level kernels
 // ---------------------------------------------------------------------------
 template <typename T>
@@ -821,6 +867,19 @@ int launch_select(const ChessState& st, const Workspace& ws, const SelParams& pr
     if (rc) return rc;
   }
   return CHESS_OK;
+}
+
+// head shard: the scan of one level with its tail exporting partial scores
+int launch_select_partial(const ChessState& st, const Workspace& ws, const SelParams& prm,
+                          int level, cudaStream_t stream) {
+  return st.d.summary_dtype == 0 ? launch_scan<float>(st, ws, prm, level, stream)
+                                 : launch_scan<double>(st, ws, prm, level, stream);
+}
+
+int launch_select_combine(const ChessState& st, const Workspace& ws, const SelParams& prm,
+                          int level, const double* gathered, int world, cudaStream_t stream) {
+  select_combine_kernel<<<st.d.batch, kNT, 0, stream>>>(st, ws, prm, level, gathered, world);
+  return check_launch("select_combine");
 }
 
 int launch_build_ws_all(const ChessState& st, cudaStream_t stream);

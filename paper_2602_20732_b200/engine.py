@@ -16,6 +16,7 @@ step is capturable as one CUDA graph (no host sync inside).
 
 from __future__ import annotations
 
+import contextlib
 import ctypes as C
 import math
 
@@ -24,6 +25,11 @@ import torch
 from . import _lib
 from .config import SelectionConfig
 from .state import DecodeState
+
+
+def _on(stream):
+    """Make `stream` torch's current stream (collectives run on it)."""
+    return torch.cuda.stream(stream) if stream is not None else contextlib.nullcontext()
 
 
 def parse_policy(policy):
@@ -63,6 +69,7 @@ class ChessDecoder:
         trigger_mode="joint",
         full_scan=False,
         softmax_scale=None,
+        exchange=None,
     ):
         from .errors import ConfigurationError
 
@@ -96,6 +103,11 @@ class ChessDecoder:
             self.trig_cfg.tau_varentropy = thresholds.tau_varentropy
         self.scale = softmax_scale if softmax_scale is not None else 1.0 / math.sqrt(s.head_dim)
         self.graph = None
+        # KV-head shard (parallel.HeadShardExchange): selection runs level by
+        # level around the partial-score all-gather; outputs are gathered per layer
+        self.exchange = exchange
+        if exchange is not None and exchange.levels != ([3] if full_scan else [0, 1, 2]):
+            raise ConfigurationError("exchange and decoder disagree on full_scan")
 
     # ------------------------------------------------------------------
     # prefill: KV rows already in the pool, page tables/counters set
@@ -106,7 +118,22 @@ class ChessDecoder:
 
     def select(self, force_all=False, stream=None):
         cfg = self.sel_cfg_all if force_all else self.sel_cfg
-        _lib.call("chess_select", self.state.ref, C.byref(cfg), _lib.stream_ptr(stream))
+        x = self.exchange
+        if x is None:
+            _lib.call("chess_select", self.state.ref, C.byref(cfg), _lib.stream_ptr(stream))
+            return
+        sp = _lib.stream_ptr(stream)
+        with _on(stream):
+            self._select_levels(cfg, sp)
+
+    def _select_levels(self, cfg, sp):
+        x = self.exchange
+        for lv in x.levels:
+            _lib.call("chess_select_partial", self.state.ref, C.byref(cfg), lv,
+                      _lib.ptr(x.partial[lv]), x.ld[lv], sp)
+            gathered = x.scores(lv)
+            _lib.call("chess_select_combine", self.state.ref, C.byref(cfg), lv,
+                      _lib.ptr(gathered), x.world, x.ld[lv], sp)
 
     def initial_selection(self, stream=None):
         """Post-prefill selection (simulate.py:147-151); 'never' keeps every page."""
@@ -148,11 +175,19 @@ class ChessDecoder:
 
     def step(self, k_new, v_new, q, logits, out, lse=None, entropy_out=None, stream=None):
         """k_new/v_new [b, D] bf16; q/out [b, L, H_q, d] bf16; logits [b, V] f32;
-        lse (optional) f32 [L, b, H_q]."""
+        lse (optional) f32 [L, b, H_q].
+
+        Head shard (self.exchange set): D, H_q are this rank's; `out` is the
+        per-layer gather buffer [L, world, b, H_q, d] — K4 writes the rank's
+        block and the exchange all-gathers it after every layer."""
+        x = self.exchange
         self.append(k_new, v_new, stream)
         for layer in range(self.state.shape.layers):
-            self.attend(layer, q[:, layer], out[:, layer],
-                        None if lse is None else lse[layer], stream)
+            o = out[:, layer] if x is None else out[layer, x.rank]
+            self.attend(layer, q[:, layer], o, None if lse is None else lse[layer], stream)
+            if x is not None:
+                with _on(stream):
+                    x.outputs(out[layer])
         self.entropy_trigger(logits, entropy_out, stream)
         self.seal(stream)
         if self.kind != "never":

@@ -80,6 +80,58 @@ class HeadShard:
         return torch.cat(cols)
 
 
+class HeadShardExchange:
+    """The two exchange steps of the KV-head-sharded decode path on NCCL.
+
+    (1) Scores: every level of the cascade (grids -> chunks of kept grids ->
+        pages of kept chunks) runs `chess_select_partial` on the rank's own
+        columns, all-gathers the f64 partial scores [batch, ld_level] into
+        [world, batch, ld_level], and `chess_select_combine` adds them in rank
+        order, so every rank takes the identical top-k and builds the
+        identical working set / block table (selection.py:62-111).
+    (2) Outputs: K4 writes the rank's query heads straight into its slot of
+        the per-layer gather buffer [world, batch, H_q/n, d]; an in-place
+        all-gather completes it (rank-major head blocks: global head
+        r*H_q/n + j is [r, :, j]).
+
+    Buffers are allocated once, so the exchange is CUDA-graph capturable.
+    `allgather` is injectable: the single-GPU tests drive several rank
+    states in one process through a local stand-in.
+    """
+
+    def __init__(self, shard: "HeadShard", batch: int, max_pages: int, pages_per_chunk: int,
+                 chunks_per_grid: int, device, group=None, full_scan=False, allgather=None):
+        import math
+
+        self.shard, self.world, self.rank, self.group = shard, shard.world, shard.rank, group
+        mc = math.ceil(max_pages / pages_per_chunk)
+        mg = math.ceil(mc / chunks_per_grid)
+        caps = {0: mg, 1: mc, 2: max_pages, 3: mg + mc + max_pages}
+        self.levels = [3] if full_scan else [0, 1, 2]
+        f64 = dict(dtype=torch.float64, device=device)
+        self.ld = {lv: caps[lv] for lv in self.levels}
+        self.partial = {lv: torch.zeros((batch, self.ld[lv]), **f64) for lv in self.levels}
+        self.gathered = {lv: torch.zeros((self.world, batch, self.ld[lv]), **f64) for lv in self.levels}
+        self._allgather = allgather or self._nccl_allgather
+
+    def _nccl_allgather(self, out: torch.Tensor, inp: torch.Tensor) -> None:
+        if self.world == 1:
+            if out.data_ptr() != inp.data_ptr():
+                out[0].copy_(inp)
+            return
+        # output as [world * rows, ...] (rank blocks concatenated on dim 0)
+        dist.all_gather_into_tensor(out.view(-1, *inp.shape[1:]), inp, group=self.group)
+
+    def scores(self, level: int) -> torch.Tensor:
+        self._allgather(self.gathered[level], self.partial[level])
+        return self.gathered[level]
+
+    def outputs(self, gather_buf: torch.Tensor) -> torch.Tensor:
+        """gather_buf [world, batch, H_q/n, d]; this rank's block is filled."""
+        self._allgather(gather_buf, gather_buf[self.rank])
+        return gather_buf
+
+
 def allgather_sum_scores(partial: torch.Tensor, group=None) -> torch.Tensor:
     """Sum of every rank's partial f64 scores, added in rank order so all
     ranks hold bit-identical results (the cascade then selects identically)."""

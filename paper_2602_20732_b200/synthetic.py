@@ -83,8 +83,16 @@ class SyntheticDecode:
 
     def __init__(self, cfg_name="cfg3", batch=None, gen_pages=128, ring=64, seed=0,
                  device="cuda", summary_dtype="f32", kv_budget_gib=None, unstable_every=2,
-                 window=4, nc=8, ng=8):
+                 window=4, nc=8, ng=8, head_shard=None):
         c = dict(CONFIGS[cfg_name])
+        if head_shard is not None:
+            # KV-head shard: this rank's kv / q heads of every layer
+            _, world = head_shard
+            if c["kv_heads"] % world or c["q_heads"] % world:
+                raise ValueError(f"{cfg_name}: heads not divisible by world={world}")
+            c["kv_heads"] //= world
+            c["q_heads"] //= world
+        self.head_shard = head_shard
         self.name = cfg_name
         self.c = c
         b = batch if batch is not None else c["batch"]

@@ -16,6 +16,7 @@ from oracle import pagesel_ref as ref
 from paper_2602_20732_b200.parallel import (
     BatchShard,
     HeadShard,
+    HeadShardExchange,
     allgather_sum_scores,
     gather_head_outputs,
     max_over_ranks,
@@ -60,6 +61,17 @@ def _worker(rank, world, port, q):
         gathered = gather_head_outputs(out_local)
         t = max_over_ranks(1.0 + rank)
         shard = BatchShard(rank, world, 5)
+        # the engine's exchange object over the same process group
+        x = HeadShardExchange(sh, 2, 37, nc, ng, "cpu")
+        for lv in x.levels:
+            x.partial[lv].fill_(10.0 * lv + rank)
+            g = x.scores(lv)
+            assert g.shape == (world, 2, x.ld[lv])
+            assert all(torch.all(g[r] == 10.0 * lv + r) for r in range(world))
+        buf = torch.zeros((world, 2, sh.local_q_heads, d))
+        buf[rank].fill_(rank + 1.0)
+        x.outputs(buf)
+        assert all(torch.all(buf[r] == r + 1.0) for r in range(world))
         q.put((rank, s.tobytes(), sel.tolist(), float(np.max(np.abs(s - full))), gathered.numpy(),
                t, list(shard.slots), cols.tolist()))
     finally:
