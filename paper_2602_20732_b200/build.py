@@ -17,6 +17,7 @@ REPO = PKG_DIR.parent
 CSRC = PKG_DIR / "csrc"
 BUILD = PKG_DIR / "_build"
 LIB = PKG_DIR / "libchess_b200.so"
+TRACE_LIB = PKG_DIR / "libchess_b200_trace.so"
 SOURCES = ["capi.cu", "k_index.cu", "k_select.cu", "k_attn.cu", "k_entropy.cu"]
 HEADERS = [CSRC / "common.cuh", REPO / "include" / "chess_b200.h"]
 
@@ -42,33 +43,39 @@ def _stale(target: Path, deps) -> bool:
     return any(Path(d).stat().st_mtime > t for d in deps)
 
 
-def build(verbose: bool = False, force: bool = False) -> Path:
-    BUILD.mkdir(exist_ok=True)
+def build(verbose: bool = False, force: bool = False, trace: bool = False) -> Path:
+    """Product library; trace=True builds the debug-timeline variant
+    (-DCHESS_TRACE=1) as libchess_b200_trace.so for the micro-benchmarks
+    (select it with CHESS_B200_LIB)."""
+    bdir = BUILD / "trace" if trace else BUILD
+    lib = TRACE_LIB if trace else LIB
+    extra = ["-DCHESS_TRACE=1"] if trace else []
+    bdir.mkdir(parents=True, exist_ok=True)
     objs = []
     for src in SOURCES:
         s = CSRC / src
-        o = BUILD / (s.stem + ".o")
+        o = bdir / (s.stem + ".o")
         objs.append(o)
         if force or _stale(o, [s, *HEADERS]):
-            cmd = [NVCC, *ARCH, *FLAGS, "-c", str(s), "-o", str(o)]
+            cmd = [NVCC, *ARCH, *FLAGS, *extra, "-c", str(s), "-o", str(o)]
             res = subprocess.run(cmd, capture_output=True, text=True)
-            log = BUILD / (s.stem + ".ptxas.log")
+            log = bdir / (s.stem + ".ptxas.log")
             log.write_text(res.stdout + res.stderr)
             if res.returncode != 0:
                 sys.stderr.write(res.stdout + res.stderr)
                 raise RuntimeError(f"nvcc failed on {src}")
             if verbose:
                 print(f"compiled {src}")
-    if force or _stale(LIB, objs):
-        cmd = [NVCC, *ARCH, "-shared", "-cudart", "static", "-o", str(LIB), *map(str, objs)]
+    if force or _stale(lib, objs):
+        cmd = [NVCC, *ARCH, "-shared", "-cudart", "static", "-o", str(lib), *map(str, objs)]
         res = subprocess.run(cmd, capture_output=True, text=True)
         if res.returncode != 0:
             sys.stderr.write(res.stdout + res.stderr)
             raise RuntimeError("nvcc link failed")
         if verbose:
-            print(f"linked {LIB}")
-    return LIB
+            print(f"linked {lib}")
+    return lib
 
 
 if __name__ == "__main__":
-    build(verbose=True, force="--force" in sys.argv)
+    build(verbose=True, force="--force" in sys.argv, trace="--trace" in sys.argv)

@@ -47,6 +47,15 @@ constexpr int kScanRows = 8;       // rows per work item
 constexpr int kScanThreads = 256;
 constexpr int kMaxBatch = 1024;
 
+// Debug timelines (per-CTA globaltimer stamps read by tools/*_micro.py).
+// Off in the product build: the stamps are global stores that every later
+// release fence in the kernel would have to wait for.  build.py builds a
+// separate libchess_b200_trace.so with -DCHESS_TRACE=1.
+#ifndef CHESS_TRACE
+#define CHESS_TRACE 0
+#endif
+constexpr bool kTrace = CHESS_TRACE != 0;
+
 struct Workspace {
   int32_t* sel_done;     // [batch]
   int32_t* cand;         // [batch][3][max_rows]  candidate row ids per level
@@ -229,6 +238,63 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     }
   }
 }
+// ---- thread-block clusters / DSMEM ----
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// shared::cta address -> shared::cluster address of the same offset in CTA `rank`
+__device__ __forceinline__ uint32_t mapa_shared(uint32_t addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void st_cluster_f32x2(uint32_t addr, float a, float b) {
+  asm volatile("st.shared::cluster.v2.f32 [%0], {%1, %2};" ::"r"(addr), "f"(a), "f"(b) : "memory");
+}
+// asynchronous 8-byte store into another CTA's shared memory that completes
+// `bytes` of the transaction count of that CTA's mbarrier (no release fence:
+// the consumer's mbarrier phase completion makes the data visible)
+__device__ __forceinline__ void st_async_f32x2(uint32_t cluster_addr, float a, float b,
+                                               uint32_t cluster_bar) {
+  asm volatile(
+      "st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f32 [%0], {%1, %2}, [%3];" ::"r"(
+          cluster_addr),
+      "f"(a), "f"(b), "r"(cluster_bar)
+      : "memory");
+}
+// arrive on an mbarrier in another CTA of the cluster, releasing this
+// thread's prior (DSMEM) writes at cluster scope
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_bar_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_bar_addr)
+               : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait_cluster(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+  const uint64_t t0 = global_ns();
+  uint32_t polls = 0;
+  while (!mbar_try_wait_cluster(bar, parity)) {
+    if ((++polls & 1023u) == 0 && global_ns() - t0 > 4000000000ull) {
+      printf("chess: cluster mbarrier wait timed out (block %d thread %d)\n", blockIdx.x, threadIdx.x);
+      asm volatile("trap;");
+    }
+  }
+}
+
 // 1-D bulk global->shared copy completing on an mbarrier (SASS: UBLKCP).
 __device__ __forceinline__ void tma_load_1d(void* dst_smem, const void* src_gmem, uint32_t bytes,
                                             uint64_t* bar) {

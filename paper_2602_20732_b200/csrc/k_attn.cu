@@ -61,18 +61,30 @@ struct AttnArgs {
   float* lse;
   float scale_log2;  // softmax_scale * log2(e)
   int layer;
-  int mode;  // debug (CHESS_ATTN_MODE): 0 normal, 1 loads only (no math), 2 math only (no K/V loads), 5 exit at entry, 6 exit after the prologue, 7 force stream-K
+  int cl;    // cluster-merge mode: CTAs per segment (= cluster size), 0 = off
+  int mode;  // debug (CHESS_ATTN_MODE): 0 normal, 1 loads only (no math), 2 math only (no K/V loads), 5 exit at entry, 6 exit after the prologue, 7 force stream-K, 8 no PDL wait (timing only: ignores the previous kernel)
 };
 
 // Debug timeline (read by chess_debug_attn_trace): per CTA globaltimer stamps
 // {entry, prologue done, first page ready, consumers done, exit}, kept for
 // the last launch of each layer parity.
-__device__ unsigned long long g_attn_trace[2][256][8];
-__device__ __forceinline__ void trace(int which, int layer) {
-  if (threadIdx.x == 0 && blockIdx.x < 256) g_attn_trace[layer & 1][blockIdx.x][which] = global_ns();
+// Stamps go to shared memory and are flushed by the last consumer warp at
+// exit, so they never sit in front of the kernel's release fences.
+__device__ unsigned long long g_attn_trace[2][256][16];
+__shared__ unsigned long long s_trace[16];
+__shared__ int s_trace_warps;
+__device__ __forceinline__ void trace(int which, int /*layer*/) {
+  if (kTrace && threadIdx.x == 0) s_trace[which] = global_ns();
+}
+__device__ __forceinline__ void trace_max(int which) {
+  if (kTrace) atomicMax(&s_trace[which], (unsigned long long)global_ns());
 }
 
-template <int HD, int GQ, int B>
+constexpr int kMaxCluster = 8;  // portable cluster size
+
+// XC: cluster-merge variant (piece mode with one segment per thread-block
+// cluster): the leader CTA owns an inbox for the other CTAs' piece states.
+template <int HD, int GQ, int B, bool XC = false>
 struct Cfg {
   static constexpr int kCB = HD / 64;                  // 128-byte column blocks
   static constexpr int kPageBytes = B * HD * 2;        // K (or V) bytes of a page
@@ -82,8 +94,10 @@ struct Cfg {
   static constexpr int kQBytes = GQ * HD * 2;          // one GQA group's q rows (bf16)
   static constexpr int kQSlots = 2;
   static constexpr int kTables = (kAttnMaxBatch + 1) * 4 * 4;
+  static constexpr int kXBytes = XC ? (kMaxCluster - 1) * GQ * kRow * 4 : 0;  // leader's inbox
   static constexpr int kMisc = kTables + 64 * 8 + 64 + 1024;  // tables, barriers, counters, align
-  static constexpr int kStagesRaw = (kSmemBudget - kStateBytes - kQSlots * kQBytes - kMisc) / kStageBytes;
+  static constexpr int kStagesRaw =
+      (kSmemBudget - kStateBytes - kQSlots * kQBytes - kXBytes - kMisc) / kStageBytes;
   static constexpr int kStages = kStagesRaw > 32 ? 32 : kStagesRaw;
   static constexpr int kMT = B / 16;                   // QK m-tiles (16 tokens each)
   static constexpr int kKS = HD / 16;                  // QK k-steps over d
@@ -91,7 +105,8 @@ struct Cfg {
   static constexpr int kPK = B / 16;                   // PV k-steps (16 tokens each)
   static constexpr int kEPL = GQ * HD / 32;            // merge: state elements per lane
   static constexpr size_t kSmem = 1024 + (size_t)kStages * kStageBytes + kStateBytes +
-                                  kQSlots * kQBytes + (2 * kStages + 2 * kQSlots) * 8 + 64 + kTables;
+                                  kQSlots * kQBytes + kXBytes + (2 * kStages + 2 * kQSlots + 1) * 8 +
+                                  64 + kTables;
   static_assert(kStages >= 4, "ring too shallow");
   static_assert(GQ <= 8, "one GQA group per n8 tile");
   static_assert(kEPL >= 2 && kEPL % 2 == 0 && HD % kEPL == 0, "merge lane mapping");
@@ -190,22 +205,32 @@ __device__ __forceinline__ void st_release_cta(int* p, int v) {
 //    and moves on; the last warp to arrive (smem atomic) merges the 8 states
 //    in warp order and writes the output, or the split-segment partial and the
 //    cross-CTA combine.  The slot is reopened via `st_next`.
-template <int HD, int GQ, int B>
+//
+// Cluster-merge variant (XC, args.cl > 1; segments * cl <= SMs): segment
+// (slot, kv head) number blockIdx.x / cl is split into cl near-equal pieces,
+// one per CTA of a thread-block cluster.  Each non-leader CTA pushes its
+// merged piece state into the leader's shared-memory inbox over DSMEM and
+// arrives on the leader's mbarrier (release.cluster); the leader merges the
+// states in cluster-rank order.  This replaces the split-segment path's
+// global partials + fences + atomics (~3 us of round trips) on small batches.
+template <int HD, int GQ, int B, bool XC>
 __global__ void __launch_bounds__(kThreads, kCtasPerSm)
     sparse_decode_kernel(ChessState st, Workspace ws, AttnArgs args,
                          const __grid_constant__ CUtensorMap kmap,
                          const __grid_constant__ CUtensorMap vmap) {
-  using C = Cfg<HD, GQ, B>;
+  using C = Cfg<HD, GQ, B, XC>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* ring = smem;
   float* stv = reinterpret_cast<float*>(ring + (size_t)C::kStages * C::kStageBytes);
   uint8_t* qbuf = reinterpret_cast<uint8_t*>(stv + kConsumers * GQ * C::kRow);
-  uint64_t* full = reinterpret_cast<uint64_t*>(qbuf + C::kQSlots * C::kQBytes);
+  float* xst = reinterpret_cast<float*>(qbuf + C::kQSlots * C::kQBytes);  // [cl-1][GQ][kRow] (XC)
+  uint64_t* full = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(xst) + C::kXBytes);
   uint64_t* empty = full + C::kStages;
   uint64_t* qfull = empty + C::kStages;
   uint64_t* qempty = qfull + C::kQSlots;
-  int* ctr = reinterpret_cast<int*>(qempty + C::kQSlots);  // [0] issued, [1] st_cnt, [2] st_next
+  uint64_t* xbar = qempty + C::kQSlots;                    // leader's inbox barrier (XC)
+  int* ctr = reinterpret_cast<int*>(xbar + 1);             // [0] issued, [1] st_cnt, [2] st_next
   int* prefix = ctr + 16;                                   // [nb + 1] pages before slot s
   int* s_np = prefix + kAttnMaxBatch + 1;                   // [nb] pages per segment of slot s
   int* s_fill = s_np + kAttnMaxBatch;                        // [nb] valid rows of the last page
@@ -220,7 +245,13 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
     prefetch_tmap(&vmap);
   }
   trace(0, args.layer);
-  if (threadIdx.x == 0 && blockIdx.x < 256) g_attn_trace[args.layer & 1][blockIdx.x][4] = 0;
+  if (kTrace && threadIdx.x == 0) {
+#pragma unroll
+    for (int i = 1; i < 16; ++i) s_trace[i] = 0;
+    s_trace_warps = 0;
+    if (blockIdx.x < 256)
+      for (int i = 0; i < 16; ++i) g_attn_trace[args.layer & 1][blockIdx.x][i] = 0;
+  }
   if (args.mode == 5) return;  // debug: launch overhead only
   // Everything up to the q load reads state that was final before the
   // previous kernel started (KV pool, block table, ws_len, fill), so the
@@ -287,12 +318,19 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
       mbar_init(&qfull[i], 1);
       mbar_init(&qempty[i], kConsumers);
     }
+    if (XC) {
+      // inbox: one local arrival + the peers' st.async bytes (o rows, m, l)
+      mbar_init(xbar, 1);
+      mbar_arrive_expect_tx(xbar, (uint32_t)(args.cl - 1) * (uint32_t)(GQ * (HD + 2) * 4));
+    }
     ctr[0] = 0;
     ctr[1] = 0;
     ctr[2] = 0;
     fence_barrier_init();
   }
   __syncthreads();
+  // the leader's inbox barrier is initialised before any peer can arrive on it
+  if (XC) cluster_sync_all();
   trace(1, args.layer);
   pdl_launch_dependents();
 
@@ -303,9 +341,21 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
   // piece mode: CTA c owns piece c of the segment-aligned split.
   const int G = kp > 0 ? ppre[nb] : min((int)gridDim.x, N);
   const int c = blockIdx.x;
-  if (c >= G) return;
   int u_begin, u_end;
-  if (kp > 0) {
+  int cs = 0, ch = 0;  // XC: this cluster's segment
+  if (XC) {
+    const int seg = c / args.cl, cr = c - seg * args.cl;
+    cs = seg / H;
+    ch = seg - cs * H;
+    if (cs >= nb) return;
+    const int np = s_np[cs];
+    if (np == 0) return;  // the whole cluster has nothing to do
+    const int base = prefix[cs] + ch * np;
+    u_begin = base + (int)((int64_t)cr * np / args.cl);
+    u_end = base + (int)((int64_t)(cr + 1) * np / args.cl);
+  } else if (c >= G) {
+    return;
+  } else if (kp > 0) {
     int lo = 0, hi = nb;
     while (hi - lo > 1) {
       const int mid = (lo + hi) >> 1;
@@ -369,7 +419,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
         auto issue_q = [&](int at) {
           const int tag = __shfl_sync(0xffffffffu, cur_tag, at);
           if (lane == 0) {
-            if (qk == 0) pdl_wait();
+            if (qk == 0 && args.mode != 8) pdl_wait();
             const int qs = qk & 1;
             mbar_wait(&qempty[qs], (uint32_t)(((qk >> 1) & 1) ^ 1));
             mbar_arrive_expect_tx(&qfull[qs], (uint32_t)C::kQBytes);
@@ -413,9 +463,17 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
   const int g = lane >> 2, t = lane & 3;
   const int lr = lane & 7, lm = lane >> 3;  // ldmatrix: row in matrix, matrix index
   int u = u_begin, k = 0;
-  while (u < u_end) {
+  bool once = XC;  // XC: exactly one piece per CTA, possibly empty (np < cl)
+  while (u < u_end || once) {
+    once = false;
     int s, h, p0;
-    locate(u, s, h, p0);
+    if (XC) {
+      s = cs;
+      h = ch;
+      p0 = u - (prefix[s] + h * s_np[s]);
+    } else {
+      locate(u, s, h, p0);
+    }
     const int np = s_np[s];
     const int seg_begin = prefix[s] + h * np;
     const int seg_end = seg_begin + np;
@@ -426,7 +484,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
 
     // q^T B-fragments from the q ring: b[ks][0] = q[g][16ks+2t..], b[ks][1] = q[g][16ks+8+2t..]
     uint32_t qb[C::kKS][2];
-    {
+    if (piece_n > 0) {
       const int qs = k & 1;
       mbar_wait(&qfull[qs], (uint32_t)((k >> 1) & 1));
       const uint8_t* qrow = qbuf + qs * C::kQBytes + g * HD * 2;
@@ -459,7 +517,10 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
       }
       __syncwarp();
       mbar_wait(&full[stage], phase);
-      if (j == 0 && warp == 0) trace(2, args.layer);
+      if (j == 0 && warp == 0) {
+        trace(2, args.layer);
+        if (kTrace && lane == 0) s_trace[8] = clock64();
+      }
       const uint32_t kst = smem_u32(ring + (size_t)stage * C::kStageBytes);
       const uint32_t vst = kst + C::kPageBytes;
       if (args.mode != 1) {
@@ -553,12 +614,15 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
     if (piece_end == u_end && warp == 0) trace(3, args.layer);
 
     // ---- hand this warp's piece state to the merge slot ----
-    if (k == 0) pdl_wait();
+    if (k == 0 && args.mode != 8) pdl_wait();
+    if (k == 0 && lane == 0) trace_max(5);  // debug timeline: last warp past the PDL wait
+    const long long ck0 = kTrace ? clock64() : 0;
     if (lane == 0) {
       while (ld_acquire_cta(&ctr[2]) != k) {
       }
     }
     __syncwarp();
+    const long long ck1 = kTrace ? clock64() : 0;
 #pragma unroll
     for (int e = 0; e < 2; ++e) {
       const int hh = 2 * t + e;
@@ -582,6 +646,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
       last = atomicAdd(&ctr[1], 1) == kConsumers - 1;
     }
     last = __shfl_sync(0xffffffffu, last, 0);
+    const long long ck2 = kTrace ? clock64() : 0;
     if (last) {
       // ---- this warp merges the piece (warp order, deterministic) ----
       __threadfence_block();
@@ -620,11 +685,56 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
         ctr[1] = 0;
         st_release_cta(&ctr[2], k + 1);
       }
+      if (lane == 0) trace_max(6);
+      const long long ck3 = kTrace ? clock64() : 0;
+      if (kTrace && lane == 0) {
+        s_trace[10] = ck1 - ck0;
+        s_trace[11] = ck2 - ck1;
+        s_trace[12] = ck3 - ck2;
+      }
       const bool whole = seg_begin >= u_begin && seg_end <= u_end;
       const int sg = s * H + h;
       __nv_bfloat16* orow = args.out + (int64_t)s * args.out_stride + ((int64_t)h * GQ + hh) * HD + el;
       float* lse = args.lse ? args.lse + (int64_t)s * d.q_heads + h * GQ + hh : nullptr;
-      if (whole) {
+      if (XC) {
+        const int cr = c % args.cl;  // == %cluster_ctarank (1-D clusters of consecutive CTAs)
+        if (cr != 0) {
+          // push (o, m, l) of this piece into the leader's inbox slot cr-1
+          // (st.async completes bytes on the leader's inbox mbarrier)
+          const uint32_t rx = mapa_shared(smem_u32(xst + ((cr - 1) * GQ + hh) * C::kRow), 0);
+          const uint32_t rb = mapa_shared(smem_u32(xbar), 0);
+#pragma unroll
+          for (int e = 0; e < C::kEPL; e += 2) st_async_f32x2(rx + (uint32_t)(el + e) * 4u, acc[e], acc[e + 1], rb);
+          if (el == 0) st_async_f32x2(rx + (uint32_t)HD * 4u, M, L, rb);
+          if (kTrace && lane == 0) s_trace[13] = clock64() - ck3;
+        } else {
+          // leader: own state first, then the peers in cluster-rank order
+          mbar_wait_cluster(xbar, 0);
+          if (lane == 0) trace_max(7);
+          float Mx = M;
+          for (int r = 1; r < args.cl; ++r) Mx = fmaxf(Mx, xst[((r - 1) * GQ + hh) * C::kRow + HD]);
+          const float f0 = M == -INFINITY ? 0.f : exp2f(M - Mx);
+          float Lx = L * f0;
+#pragma unroll
+          for (int e = 0; e < C::kEPL; ++e) acc[e] *= f0;
+          for (int r = 1; r < args.cl; ++r) {
+            const float* pr = xst + ((r - 1) * GQ + hh) * C::kRow;
+            const float f = pr[HD] == -INFINITY ? 0.f : exp2f(pr[HD] - Mx);
+            Lx = fmaf(pr[HD + 1], f, Lx);
+#pragma unroll
+            for (int e = 0; e < C::kEPL; e += 2) {
+              const float2 x = *reinterpret_cast<const float2*>(pr + el + e);
+              acc[e] = fmaf(x.x, f, acc[e]);
+              acc[e + 1] = fmaf(x.y, f, acc[e + 1]);
+            }
+          }
+          const float inv = 1.f / Lx;
+#pragma unroll
+          for (int e = 0; e < C::kEPL; e += 2)
+            *reinterpret_cast<__nv_bfloat162*>(orow + e) = __floats2bfloat162_rn(acc[e] * inv, acc[e + 1] * inv);
+          if (lse && el == 0) *lse = (Mx + log2f(Lx)) * kLn2;
+        }
+      } else if (whole) {
         const float inv = 1.f / L;
 #pragma unroll
         for (int e = 0; e < C::kEPL; e += 2)
@@ -713,7 +823,12 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
     ++k;
   }
   // exit stamp: the last consumer warp to finish (merges included)
-  if (lane == 0 && blockIdx.x < 256) atomicMax(&g_attn_trace[args.layer & 1][blockIdx.x][4], (unsigned long long)global_ns());
+  if (kTrace && lane == 0) {
+    trace_max(4);
+    atomicMax(&s_trace[9], (unsigned long long)clock64());
+    if (atomicAdd(&s_trace_warps, 1) == kConsumers - 1 && blockIdx.x < 256)
+      for (int i = 0; i < 16; ++i) g_attn_trace[args.layer & 1][blockIdx.x][i] = s_trace[i];
+  }
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
@@ -750,12 +865,86 @@ int make_kv_map(CUtensorMap* m, const void* base, const ChessDims& d) {
 }
 
 template <int HD, int GQ, int B>
-int launch_inst(const ChessState& st, const Workspace& ws, const AttnArgs& args, int nctas,
+int launch_cluster(const ChessState& st, const Workspace& ws, const AttnArgs& args, int segs,
+                   cudaStream_t stream) {
+  using C = Cfg<HD, GQ, B, true>;
+  auto kfn = sparse_decode_kernel<HD, GQ, B, true>;  // smem attribute set by cluster_size_for
+  CUtensorMap km, vm;
+  int rc = make_kv_map(&km, st.k_pool, st.d);
+  if (rc) return rc;
+  rc = make_kv_map(&vm, st.v_pool, st.d);
+  if (rc) return rc;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(segs * args.cl);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = C::kSmem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = args.cl;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  static const bool no_pdl = getenv("CHESS_ATTN_NOPDL") != nullptr;  // debug A/B
+  cfg.numAttrs = no_pdl ? 1 : 2;
+  cudaLaunchKernelEx(&cfg, kfn, st, ws, args, km, vm);
+  return check_launch("sparse_decode(cluster)");
+}
+
+template <int HD, int GQ, int B>
+int cluster_size_for(int segs);
+
+// Largest cluster size (8, 4, 2) whose clusters can all be co-resident for
+// `segs` segments, or 0 (no cluster mode: batch * kv_heads > SMs / 2).
+template <int HD, int GQ, int B>
+int cluster_size_for(int segs) {
+  static int max_active[kMaxCluster + 1] = {};
+  static bool probed = false;
+  auto kfn = sparse_decode_kernel<HD, GQ, B, true>;
+  using C = Cfg<HD, GQ, B, true>;
+  if (!probed) {
+    cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::kSmem);
+    for (int cl = 2; cl <= kMaxCluster; cl *= 2) {
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(cl * 8);
+      cfg.blockDim = dim3(kThreads);
+      cfg.dynamicSmemBytes = C::kSmem;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeClusterDimension;
+      attr[0].val.clusterDim.x = cl;
+      attr[0].val.clusterDim.y = 1;
+      attr[0].val.clusterDim.z = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      int n = 0;
+      if (cudaOccupancyMaxActiveClusters(&n, kfn, &cfg) != cudaSuccess) {
+        cudaGetLastError();
+        n = 0;
+      }
+      max_active[cl] = n;
+    }
+    probed = true;
+  }
+  static const bool off = getenv("CHESS_ATTN_CLUSTER") && atoi(getenv("CHESS_ATTN_CLUSTER")) == 0;  // A/B
+  if (off || segs <= 0) return 0;
+  for (int cl = kMaxCluster; cl >= 2; cl /= 2)
+    if (segs <= max_active[cl] && segs * cl <= num_sms()) return cl;
+  return 0;
+}
+
+template <int HD, int GQ, int B>
+int launch_inst(const ChessState& st, const Workspace& ws, const AttnArgs& args_in, int nctas,
                 cudaStream_t stream) {
+  AttnArgs args = args_in;
+  const int segs = st.d.batch * st.d.kv_heads;
+  args.cl = args.mode == 7 ? 0 : cluster_size_for<HD, GQ, B>(segs);
+  if (args.cl) return launch_cluster<HD, GQ, B>(st, ws, args, segs, stream);
   using C = Cfg<HD, GQ, B>;
   const size_t smem = C::kSmem;
   static bool configured = false;
-  auto kfn = sparse_decode_kernel<HD, GQ, B>;
+  auto kfn = sparse_decode_kernel<HD, GQ, B, false>;
   if (!configured) {
     cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     configured = true;
@@ -801,6 +990,7 @@ int launch_sparse_decode(const ChessState& st, const Workspace& ws, int layer, c
   a.layer = layer;
   static const int dbg_mode = getenv("CHESS_ATTN_MODE") ? atoi(getenv("CHESS_ATTN_MODE")) : 0;
   a.mode = dbg_mode;
+  a.cl = 0;
   const int gq = d.q_heads / d.kv_heads;
   const int nctas = ws.attn_ctas;
   if ((reinterpret_cast<uintptr_t>(q) & 15) || (q_stride & 7))
@@ -831,7 +1021,7 @@ int launch_sparse_decode(const ChessState& st, const Workspace& ws, int layer, c
 }  // namespace chess
 
 // Debug only (not part of include/chess_b200.h): copy the per-CTA timeline of
-// the last sparse_decode launch of each layer parity, [2][256][8] u64 ns.
+// the last sparse_decode launch of each layer parity, [2][256][16] u64 (ns; [8],[9] SM clocks).
 extern "C" int chess_debug_attn_trace(unsigned long long* host_out) {
   return cudaMemcpyFromSymbol(host_out, chess::g_attn_trace, sizeof(chess::g_attn_trace)) == cudaSuccess ? 0 : 8;
 }

@@ -110,7 +110,7 @@ constexpr int kTailCap = 1024;  // candidates whose keys / flags stay in shared 
 // {flush entered, counter won, scores reduced, level-0 top-k, done}.
 __device__ unsigned long long g_tail_trace[4][64][8];
 __device__ __forceinline__ void tail_trace(int level, int s, int which) {
-  if (threadIdx.x == 0 && s < 64) g_tail_trace[level][s][which] = global_ns();
+  if (kTrace && threadIdx.x == 0 && s < 64) g_tail_trace[level][s][which] = global_ns();
 }
 struct TailSmem {
   int hist[256];
@@ -287,7 +287,7 @@ constexpr int kScanCTA = kNT + 32;  // 8 consumer warps + 1 producer warp
 // warp 0, rows consumed}.
 __device__ unsigned long long g_sel_trace[4][256][8];
 __device__ __forceinline__ void sel_trace(int level, int which, unsigned long long v) {
-  if (blockIdx.x < 256) g_sel_trace[level][blockIdx.x][which] = v;
+  if (kTrace && blockIdx.x < 256) g_sel_trace[level][blockIdx.x][which] = v;
 }
 
 template <typename T>
@@ -481,7 +481,7 @@ __global__ void __launch_bounds__(kScanCTA, 1) select_scan_kernel(ChessState st,
     block_sync<kNT>();
     if (s_last) {
       fence_acq_rel_gpu();
-      if (threadIdx.x == 0 && s_done < 64) g_tail_trace[level][s_done][0] = tf;
+      if (kTrace && threadIdx.x == 0 && s_done < 64) g_tail_trace[level][s_done][0] = tf;
       tail_trace(level, s_done, 1);
       select_tail(st, ws, prm, s_done, level, s_rows[s_done], sm);
       tail_trace(level, s_done, 4);

@@ -95,17 +95,27 @@ def main():
                         "graph_GBps": bytes_launch / us_g / 1e3}
         # per-CTA timelines of the last two launches of the graph (layers L-2, L-1)
         import ctypes
-        buf = (ctypes.c_ulonglong * (2 * 256 * 8))()
+        buf = (ctypes.c_ulonglong * (2 * 256 * 16))()
         if _lib.load().chess_debug_attn_trace(buf) == 0:
-            tr = np.frombuffer(buf, dtype=np.uint64).reshape(2, 256, 8).astype(np.int64)
+            tr = np.frombuffer(buf, dtype=np.uint64).reshape(2, 256, 16).astype(np.int64)
             ta, tb = tr[(L - 2) & 1], tr[(L - 1) & 1]
             ok_a, ok_b = ta[:, 4] > ta[:, 0], tb[:, 4] > tb[:, 0]
+            if not ok_a.any() or not ok_b.any():
+                print(json.dumps(res))
+                continue
             t0 = ta[ok_a, 0].min()
             pct = lambda x: [round(float(np.percentile((x - t0) / 1e3, p)), 2) for p in (0, 50, 100)]
             res[pattern]["trace_us"] = {
                 "prev_entry": pct(ta[ok_a, 0]), "prev_exit": pct(ta[ok_a, 4]),
                 "entry": pct(tb[ok_b, 0]), "prologue": pct(tb[ok_b, 1]),
-                "exit": pct(tb[ok_b, 4])}
+                "first_page": pct(tb[ok_b & (tb[:, 2] > 0), 2]) if (ok_b & (tb[:, 2] > 0)).any() else None,
+                "consumed": pct(tb[ok_b & (tb[:, 3] > 0), 3]) if (ok_b & (tb[:, 3] > 0)).any() else None,
+                "exit": pct(tb[ok_b, 4]),
+                "pdl_passed": pct(tb[ok_b & (tb[:, 5] > 0), 5]) if (ok_b & (tb[:, 5] > 0)).any() else None,
+                "merged": pct(tb[ok_b & (tb[:, 6] > 0), 6]) if (ok_b & (tb[:, 6] > 0)).any() else None,
+                "sm_mhz": (lambda m: round(float(np.median((tb[m, 9] - tb[m, 8]) / (tb[m, 4] - tb[m, 2]) * 1e3)), 0) if m.any() else None)(ok_b & (tb[:, 8] > 0) & (tb[:, 4] > tb[:, 2])),
+                "cycles_spin_write_merge_push_arrive": [int(np.median(tb[ok_b & (tb[:, i] > 0), i])) if (ok_b & (tb[:, i] > 0)).any() else None for i in range(10, 15)],
+                "inbox": pct(tb[ok_b & (tb[:, 7] > 0), 7]) if (ok_b & (tb[:, 7] > 0)).any() else None}
     res["bytes_per_launch"] = bytes_launch
     print(json.dumps(res))
 
