@@ -75,7 +75,7 @@ struct Workspace {
   int32_t n_slices;
 };
 
-constexpr int kEntSplit = 16;
+constexpr int kEntSplit = 64;  // max CTAs per logit row (entropy split partials)
 constexpr int kAttnCtasMax = 160;               // attention CTAs (<= SMs)
 constexpr int kAttnWarpsMax = kAttnCtasMax * 8; // stream-K warps (partial slots)
 
@@ -371,11 +371,13 @@ __device__ __forceinline__ int block_exclusive_scan(int v, int* smem_warp, int* 
   return base + x - v;
 }
 
+constexpr int kRankTopkMax = 64;  // rank-count top-k up to this many candidates
+
 // Block-wide top-k selection over n keys (keys[i] = score_key(score), entries
 // in increasing index order).  Marks keep[i] = 1 for exactly min(k, n)
 // entries: all keys above the k-th largest key, plus the lowest-index entries
 // equal to it (ties to the lower index, selection.py:77-88).  Radix select
-// over 8 digits of 8 bits.  smem: 256 ints hist + 40 ints scratch.
+// over the differing digits of 8 bits.  smem: 256 ints hist + 40 ints scratch.
 template <int NT>
 __device__ void block_topk_mark(const uint64_t* keys, int n, int k, int* keep, int* s_hist,
                                 int* s_scratch) {
@@ -389,19 +391,77 @@ __device__ void block_topk_mark(const uint64_t* keys, int n, int k, int* keep, i
     block_sync<NT>();
     return;
   }
-  uint64_t prefix = 0, mask = 0;
+  if (n <= kRankTopkMax) {
+    // tiny candidate sets: keep[i] = rank_i < k, rank_i = #{j: key_j > key_i,
+    // or equal and j < i} (the stable argsort order, ties to the lower index)
+    for (int i = threadIdx.x; i < n; i += NT) {
+      const uint64_t ki = keys[i];
+      int rank = 0;
+#pragma unroll 4
+      for (int j = 0; j < n; ++j) {
+        const uint64_t kj = keys[j];
+        rank += (kj > ki || (kj == ki && j < i)) ? 1 : 0;
+      }
+      keep[i] = rank < k ? 1 : 0;
+    }
+    block_sync<NT>();
+    return;
+  }
+  // Radix select.  Digits above the first byte where the smallest and largest
+  // key differ are common to every key and skipped; histogram increments are
+  // warp-aggregated (match.any), so equal digits do not serialise on one bin.
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint64_t kmin = ~0ull, kmax = 0ull;
+  for (int i = threadIdx.x; i < n; i += NT) {
+    const uint64_t x = keys[i];
+    kmin = x < kmin ? x : kmin;
+    kmax = x > kmax ? x : kmax;
+  }
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) {
+    const uint64_t a = __shfl_xor_sync(0xffffffffu, kmin, o), b = __shfl_xor_sync(0xffffffffu, kmax, o);
+    kmin = a < kmin ? a : kmin;
+    kmax = b > kmax ? b : kmax;
+  }
+  uint64_t* s_mm = reinterpret_cast<uint64_t*>(s_hist);  // [NT/32][2] (hist is reset below)
+  if (lane == 0) {
+    s_mm[2 * warp] = kmin;
+    s_mm[2 * warp + 1] = kmax;
+  }
+  block_sync<NT>();
+  uint64_t gmin = s_mm[0], gmax = s_mm[1];
+  for (int w = 1; w < NT / 32; ++w) {
+    gmin = s_mm[2 * w] < gmin ? s_mm[2 * w] : gmin;
+    gmax = s_mm[2 * w + 1] > gmax ? s_mm[2 * w + 1] : gmax;
+  }
+  block_sync<NT>();
+  const uint64_t diff = gmin ^ gmax;
+  if (diff == 0) {  // every key equal: the k lowest indices
+    for (int i = threadIdx.x; i < n; i += NT) keep[i] = i < k ? 1 : 0;
+    block_sync<NT>();
+    return;
+  }
+  const int top_shift = ((63 - __clzll((long long)diff)) / 8) * 8;
+  uint64_t mask = top_shift == 56 ? 0ull : ~0ull << (top_shift + 8);
+  uint64_t prefix = gmax & mask;
   int kk = k;  // how many still to take among keys matching prefix
-  for (int shift = 56; shift >= 0; shift -= 8) {
+  for (int shift = top_shift; shift >= 0; shift -= 8) {
     for (int b = threadIdx.x; b < 256; b += NT) s_hist[b] = 0;
     block_sync<NT>();
-    for (int i = threadIdx.x; i < n; i += NT) {
-      uint64_t key = keys[i];
-      if ((key & mask) == prefix) atomicAdd(&s_hist[(key >> shift) & 255], 1);
+    for (int i0 = 0; i0 < n; i0 += NT) {
+      const int i = i0 + threadIdx.x;
+      const uint64_t key = i < n ? keys[i] : 0ull;
+      const bool in = i < n && (key & mask) == prefix;
+      const unsigned active = __ballot_sync(0xffffffffu, in);
+      if (in) {
+        const int digit = (int)((key >> shift) & 255);
+        const unsigned peers = __match_any_sync(active, digit);
+        if (lane == __ffs(peers) - 1) atomicAdd(&s_hist[digit], __popc(peers));
+      }
     }
     block_sync<NT>();
     if (threadIdx.x < 32) {
       // lane l owns bins [255-8l-7, 255-8l] (descending digit order)
-      const int lane = threadIdx.x;
       int c[8];
       int tot = 0;
 #pragma unroll
@@ -469,24 +529,19 @@ __device__ void block_build_ws(const ChessState& st, int s, int* s_scratch) {
   const int w0 = max(0, n - d.window_pages);
   const int c0 = max(w0, ns);
   const int32_t* sem = st.semantic + (int64_t)s * d.max_pages;
-  if (threadIdx.x == 0) {
-    const int nsem = st.n_semantic[s];
-    int lo = 0, hi = nsem;
-    while (lo < hi) {  // first entry >= ns
-      int mid = (lo + hi) >> 1;
-      if (sem[mid] < ns) lo = mid + 1; else hi = mid;
-    }
-    int a = lo;
-    hi = nsem;
-    while (lo < hi) {  // first entry >= w0
-      int mid = (lo + hi) >> 1;
-      if (sem[mid] < w0) lo = mid + 1; else hi = mid;
-    }
-    s_scratch[0] = a;
-    s_scratch[1] = max(a, lo);
+  // sem is sorted: lo = #entries < ns, hi = max(lo, #entries < w0), counted
+  // in parallel (one round of loads instead of two dependent binary searches)
+  const int nsem = st.n_semantic[s];
+  int c_ns = 0, c_w0 = 0;
+  for (int i = threadIdx.x; i < nsem; i += NT) {
+    const int v = sem[i];
+    c_ns += v < ns ? 1 : 0;
+    c_w0 += v < w0 ? 1 : 0;
   }
-  block_sync<NT>();
-  const int lo = s_scratch[0], hi = s_scratch[1];
+  int t_ns, t_w0;
+  block_exclusive_scan<NT>(c_ns, s_scratch, &t_ns);
+  block_exclusive_scan<NT>(c_w0, s_scratch, &t_w0);
+  const int lo = t_ns, hi = max(t_ns, t_w0);
   int total = ns + (hi - lo) + (n - c0);
   const int cap = d.max_ws;
   int32_t* wl = st.ws_logical + (int64_t)s * cap;

@@ -62,6 +62,7 @@ struct AttnArgs {
   float scale_log2;  // softmax_scale * log2(e)
   int layer;
   int cl;    // cluster-merge mode: CTAs per segment (= cluster size), 0 = off
+  int prefetch;  // pages past the first run prefetched into L2 before the PDL wait
   int mode;  // debug (CHESS_ATTN_MODE): 0 normal, 1 loads only (no math), 2 math only (no K/V loads), 5 exit at entry, 6 exit after the prologue, 7 force stream-K, 8 no PDL wait (timing only: ignores the previous kernel)
 };
 
@@ -154,6 +155,14 @@ __device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map
       "%3, %4}], [%5];" ::"r"(dst),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(bar)
       : "memory");
+}
+
+// L2 prefetch of one tensor box (no shared-memory destination, no barrier)
+__device__ __forceinline__ void tma_prefetch_4d(const CUtensorMap* map, int c0, int c1, int c2, int c3) {
+  asm volatile("cp.async.bulk.prefetch.tensor.4d.L2.global.tile [%0, {%1, %2, %3, %4}];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+               : "memory");
 }
 
 __device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
@@ -418,6 +427,22 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
         const bool first_run = qk == 0 && base == 0 && c0 == 0;
         auto issue_q = [&](int at) {
           const int tag = __shfl_sync(0xffffffffu, cur_tag, at);
+          if (qk == 0 && args.prefetch > 0 && args.mode != 2) {
+            // Before waiting on the previous grid, pull this CTA's next pages
+            // (after the first run, which is already in flight) into L2, so
+            // HBM streams through the previous layer's drain and this
+            // layer's ring refills hit L2.  Rows of pages 0..31 are in
+            // cur_row, 32..63 in nxt_row (fetched a batch ahead).
+            const int lim = min(n, kRun + args.prefetch);
+            if (lane >= kRun && lane < lim) {
+              tma_prefetch_4d(&kmap, 0, cur_row, 0, args.layer);
+              tma_prefetch_4d(&vmap, 0, cur_row, 0, args.layer);
+            }
+            if (32 + lane < lim) {
+              tma_prefetch_4d(&kmap, 0, nxt_row, 0, args.layer);
+              tma_prefetch_4d(&vmap, 0, nxt_row, 0, args.layer);
+            }
+          }
           if (lane == 0) {
             if (qk == 0 && args.mode != 8) pdl_wait();
             const int qs = qk & 1;
@@ -991,6 +1016,10 @@ int launch_sparse_decode(const ChessState& st, const Workspace& ws, int layer, c
   static const int dbg_mode = getenv("CHESS_ATTN_MODE") ? atoi(getenv("CHESS_ATTN_MODE")) : 0;
   a.mode = dbg_mode;
   a.cl = 0;
+  // measured (tools/attn_prefetch_sweep.sh): 16 pages -1% at cfg3, worse at
+  // cfg4/cfg5 and beyond 16 pages (the prefetches evict the running layer)
+  static const int prefetch = getenv("CHESS_ATTN_PREFETCH") ? atoi(getenv("CHESS_ATTN_PREFETCH")) : 0;
+  a.prefetch = prefetch;
   const int gq = d.q_heads / d.kv_heads;
   const int nctas = ws.attn_ctas;
   if ((reinterpret_cast<uintptr_t>(q) & 15) || (q_stride & 7))

@@ -7,10 +7,13 @@
 //   check_trigger      uncertainty.py:86-98   strict joint / any
 //   policy cadence     simulate.py:163-170    never/always/fixed(N)/dynamic
 // The reference consumes probabilities; the device consumes the step's fp32
-// logits and computes H(softmax(logits)) in one HBM pass: per CTA slice
-// (max, sum e, sum e*(x-max)) with f64 accumulation, merged in fixed order.
+// logits and computes H(softmax(logits)) in one HBM pass: online per-thread
+// (max, sum e, sum e*(x-max)), merged in a fixed tree per CTA and per row.
 // Page statistics use NumPy's pairwise summation order so decisions are
 // bit-identical given identical per-token entropies.
+#include <algorithm>
+#include <type_traits>
+
 #include "common.cuh"
 
 namespace chess {
@@ -27,19 +30,6 @@ struct EntArgs {
   ChessTriggerCfg cfg; // used when with_state
 };
 
-__device__ __forceinline__ void merge_msT(double& M, double& S, double& T, double m2, double s2,
-                                          double t2) {
-  if (s2 == 0.0) return;
-  if (S == 0.0) {
-    M = m2; S = s2; T = t2;
-    return;
-  }
-  const double Mn = fmax(M, m2);
-  const double f1 = exp(M - Mn), f2 = exp(m2 - Mn);
-  T = (T + S * (M - Mn)) * f1 + (t2 + s2 * (m2 - Mn)) * f2;
-  S = S * f1 + s2 * f2;
-  M = Mn;
-}
 
 // Page statistics + trigger + policy for slot s (thread 0 only).
 __device__ void page_trigger(const ChessState& st, const ChessTriggerCfg& cfg, int s) {
@@ -78,11 +68,42 @@ __device__ void page_trigger(const ChessState& st, const ChessTriggerCfg& cfg, i
   st.fire[s] = fire;
 }
 
-// grid: (kEntSplit, rows).  with_state: append H to the slot's entropy ring and
-// run the page trigger when the tail just sealed.
+// (m, S, T) with S = sum e^(x-m), T = sum e^(x-m) (x-m): merge two partial
+// triples (float factors; the |dH| bar is 1e-4 nats)
+struct MST {
+  float m, S, T;
+};
+__device__ __forceinline__ MST mst_merge(MST a, MST b) {
+  if (b.S == 0.f) return a;
+  if (a.S == 0.f) return b;
+  const float mn = fmaxf(a.m, b.m);
+  const float da = a.m - mn, db = b.m - mn;
+  const float fa = exp2f(da * 1.4426950408889634f), fb = exp2f(db * 1.4426950408889634f);
+  MST r;
+  r.m = mn;
+  r.T = fmaf(a.S, da, a.T) * fa + fmaf(b.S, db, b.T) * fb;
+  r.S = a.S * fa + b.S * fb;
+  return r;
+}
+__device__ __forceinline__ MST mst_shfl_xor(MST v, int o) {
+  MST r;
+  r.m = __shfl_xor_sync(0xffffffffu, v.m, o);
+  r.S = __shfl_xor_sync(0xffffffffu, v.S, o);
+  r.T = __shfl_xor_sync(0xffffffffu, v.T, o);
+  return r;
+}
+
+constexpr int kEntVec = 8;  // float4 per thread per chunk (held in registers)
+
+// grid: (splits, rows).  One HBM pass: each thread keeps an online (m, S, T)
+// over register-resident chunks of its slice, the CTA merges its threads in a
+// fixed shuffle tree, and the last CTA of a row merges the row's split
+// partials (one per lane, fixed tree) into H = ln S - T/S.  with_state:
+// append H to the slot's entropy ring and run the page trigger when the tail
+// just sealed.
 template <bool kWithState>
 __global__ void __launch_bounds__(kNT) entropy_kernel(ChessState st, Workspace ws, EntArgs a) {
-  __shared__ double s_red[3][kNT / 32];
+  __shared__ MST s_w[kNT / 32];
   __shared__ int s_last;
   const int r = blockIdx.y;
   const int split = blockIdx.x;
@@ -93,86 +114,90 @@ __global__ void __launch_bounds__(kNT) entropy_kernel(ChessState st, Workspace w
   const bool vec = ((a.ld & 3) == 0) && ((reinterpret_cast<uintptr_t>(a.logits) & 15) == 0);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 
-  // pass 1: max
-  float mx = -INFINITY;
-  if (vec) {
-    for (int64_t i = lo + 4 * threadIdx.x; i < hi; i += 4 * kNT) {
-      if (i + 3 < hi) {
-        const float4 v = __ldcs(reinterpret_cast<const float4*>(row + i));
-        mx = fmaxf(mx, fmaxf(fmaxf(v.x, v.y), fmaxf(v.z, v.w)));
-      } else {
-        for (int64_t j = i; j < hi; ++j) mx = fmaxf(mx, row[j]);
+  MST t = {-INFINITY, 0.f, 0.f};
+  // fold N register values into the thread's running (m, S, T)
+  auto absorb = [&](const float (&v)[4 * kEntVec], auto n_const) {
+    constexpr int N = decltype(n_const)::value;
+    float cm = -INFINITY;
+#pragma unroll
+    for (int i = 0; i < N; ++i) cm = fmaxf(cm, v[i]);
+    if (cm == -INFINITY) return;
+    const float mn = fmaxf(t.m, cm);
+    if (t.S != 0.f && mn > t.m) {  // rescale the running sums to the new max
+      const float d = t.m - mn, f = exp2f(d * 1.4426950408889634f);
+      t.T = fmaf(t.S, d, t.T) * f;
+      t.S *= f;
+    }
+    t.m = mn;
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      const float dx = v[i] - mn;
+      const float e = exp2f(dx * 1.4426950408889634f);
+      if (e > 0.f) {
+        t.S += e;
+        t.T = fmaf(e, dx, t.T);
       }
+    }
+  };
+  if (vec) {
+    constexpr int kChunk = 4 * kEntVec * kNT;
+    for (int64_t c0 = lo; c0 < hi; c0 += kChunk) {
+      float v[4 * kEntVec];
+#pragma unroll
+      for (int q = 0; q < kEntVec; ++q) {
+        const int64_t i = c0 + 4 * ((int64_t)q * kNT + threadIdx.x);
+        float4 x = make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+        if (i + 3 < hi) {
+          x = __ldcs(reinterpret_cast<const float4*>(row + i));
+        } else if (i < hi) {
+          x.x = row[i];
+          if (i + 1 < hi) x.y = row[i + 1];
+          if (i + 2 < hi) x.z = row[i + 2];
+        }
+        v[4 * q] = x.x;
+        v[4 * q + 1] = x.y;
+        v[4 * q + 2] = x.z;
+        v[4 * q + 3] = x.w;
+      }
+      absorb(v, std::integral_constant<int, 4 * kEntVec>{});
     }
   } else {
-    for (int64_t i = lo + threadIdx.x; i < hi; i += kNT) mx = fmaxf(mx, row[i]);
-  }
-#pragma unroll
-  for (int o = 16; o >= 1; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-  if (lane == 0) s_red[0][warp] = mx;
-  __syncthreads();
-  float M = s_red[0][0];
-  for (int w = 1; w < kNT / 32; ++w) M = fmaxf(M, s_red[0][w]);
-  __syncthreads();
-
-  // pass 2 (slice is L1/L2 resident): sum e^(x-M), sum e^(x-M) (x-M) in f64
-  double S = 0.0, T = 0.0;
-  const double Md = (double)M;
-  auto acc = [&](float x) {
-    const double dx = (double)x - Md;
-    const double e = (double)expf((float)dx);
-    S += e;
-    T = fma(e, dx, T);
-  };
-  if (M > -INFINITY) {
-    if (vec) {
-      for (int64_t i = lo + 4 * threadIdx.x; i < hi; i += 4 * kNT) {
-        if (i + 3 < hi) {
-          const float4 v = *reinterpret_cast<const float4*>(row + i);
-          acc(v.x); acc(v.y); acc(v.z); acc(v.w);
-        } else {
-          for (int64_t j = i; j < hi; ++j) acc(row[j]);
-        }
-      }
-    } else {
-      for (int64_t i = lo + threadIdx.x; i < hi; i += kNT) acc(row[i]);
+    for (int64_t i = lo + threadIdx.x; i < hi; i += kNT) {
+      float v[4 * kEntVec];
+      v[0] = row[i];
+      absorb(v, std::integral_constant<int, 1>{});
     }
   }
 #pragma unroll
-  for (int o = 16; o >= 1; o >>= 1) {
-    S += shfl_xor_d(S, o);
-    T += shfl_xor_d(T, o);
-  }
-  if (lane == 0) {
-    s_red[1][warp] = S;
-    s_red[2][warp] = T;
-  }
+  for (int o = 16; o >= 1; o >>= 1) t = mst_merge(t, mst_shfl_xor(t, o));
+  if (lane == 0) s_w[warp] = t;
   __syncthreads();
   if (threadIdx.x == 0) {
-    double Sb = s_red[1][0], Tb = s_red[2][0];
-    for (int w = 1; w < kNT / 32; ++w) {
-      Sb += s_red[1][w];
-      Tb += s_red[2][w];
-    }
+    MST c = s_w[0];
+    for (int w = 1; w < kNT / 32; ++w) c = mst_merge(c, s_w[w]);
     double* part = ws.ent_part + ((int64_t)r * kEntSplit + split) * 3;
-    part[0] = (double)M;
-    part[1] = Sb;
-    part[2] = Tb;
+    part[0] = (double)c.m;
+    part[1] = (double)c.S;
+    part[2] = (double)c.T;
     fence_acq_rel_gpu();
     const int prev = atomicAdd(&ws.ent_done[r], 1);
     s_last = (prev == nsplit - 1);
   }
   __syncthreads();
-  if (!s_last || threadIdx.x != 0) return;
+  if (!s_last || warp != 0) return;
   fence_acq_rel_gpu();
-  ws.ent_done[r] = 0;
-  double Mt = 0.0, St = 0.0, Tt = 0.0;
-  for (int q = 0; q < nsplit; ++q) {
+  // warp 0 merges the row's split partials: lane i owns splits i and i + 32
+  MST c = {-INFINITY, 0.f, 0.f};
+  for (int q = lane; q < nsplit; q += 32) {
     const double* part = ws.ent_part + ((int64_t)r * kEntSplit + q) * 3;
-    merge_msT(Mt, St, Tt, __ldcg(part), __ldcg(part + 1), __ldcg(part + 2));
+    c = mst_merge(c, MST{(float)__ldcg(part), (float)__ldcg(part + 1), (float)__ldcg(part + 2)});
   }
-  // H = ln S - T/S  (p = e^(x-M)/S, ln p = (x-M) - ln S)
-  double H = log(St) - Tt / St;
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) c = mst_merge(c, mst_shfl_xor(c, o));
+  if (lane != 0) return;
+  ws.ent_done[r] = 0;
+  // H = ln S - T/S  (p = e^(x-m)/S, ln p = (x-m) - ln S)
+  double H = log((double)c.S) - (double)c.T / (double)c.S;
   if (H < 0.0) H = 0.0;
   if (a.out) a.out[r] = H;
   if constexpr (kWithState) {
@@ -182,6 +207,14 @@ __global__ void __launch_bounds__(kNT) entropy_kernel(ChessState st, Workspace w
     st.ent_count[r] = pos + 1;
     page_trigger(st, a.cfg, r);
   }
+}
+
+// CTAs per row: enough to fill the GPU twice for small batches, and slices of
+// at most 4 register chunks per thread
+int ent_splits(int64_t rows, int64_t vocab) {
+  const int64_t by_gpu = (2 * (int64_t)num_sms() + rows - 1) / std::max<int64_t>(rows, 1);
+  const int64_t by_vocab = (vocab + 4 * 4 * kEntVec * kNT - 1) / (4 * 4 * kEntVec * kNT);
+  return (int)std::min<int64_t>(kEntSplit, std::max<int64_t>({(int64_t)4, by_gpu, by_vocab}));
 }
 
 // record given entropies + trigger, one thread per slot
@@ -249,7 +282,7 @@ int launch_entropy_trigger(const ChessState& st, const Workspace& ws, const floa
                            int64_t vocab, int64_t ld, const ChessTriggerCfg& cfg, double* out,
                            cudaStream_t stream) {
   EntArgs a{logits, vocab, ld, out, cfg};
-  entropy_kernel<true><<<dim3(kEntSplit, st.d.batch), kNT, 0, stream>>>(st, ws, a);
+  entropy_kernel<true><<<dim3(ent_splits(st.d.batch, vocab), st.d.batch), kNT, 0, stream>>>(st, ws, a);
   return check_launch("entropy_trigger");
 }
 
@@ -263,7 +296,7 @@ int launch_entropy_logits(const Workspace& ws, const float* logits, int64_t rows
                           int64_t ld, double* out, cudaStream_t stream) {
   EntArgs a{logits, vocab, ld, out, ChessTriggerCfg{}};
   ChessState dummy{};
-  entropy_kernel<false><<<dim3(kEntSplit, (unsigned)rows), kNT, 0, stream>>>(dummy, ws, a);
+  entropy_kernel<false><<<dim3(ent_splits(rows, vocab), (unsigned)rows), kNT, 0, stream>>>(dummy, ws, a);
   return check_launch("entropy_logits");
 }
 

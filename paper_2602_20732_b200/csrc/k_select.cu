@@ -150,18 +150,17 @@ __device__ void select_tail(const ChessState& st, const Workspace& ws, const Sel
   // a row are loaded together (one round trip) when ns <= 16
   for (int i = threadIdx.x; i < n; i += kNT) {
     const double* pr = part + (int64_t)i * ns;
-    double acc;
-    if (ns <= 16) {
+    // 16 slice partials per round trip, added in slice order
+    double acc = 0.0;
+    for (int q0 = 0; q0 < ns; q0 += 16) {
       double v[16];
 #pragma unroll
-      for (int q = 0; q < 16; ++q) v[q] = q < ns ? __ldcg(pr + q) : 0.0;
-      acc = v[0];
+      for (int q = 0; q < 16; ++q) v[q] = q0 + q < ns ? __ldcg(pr + q0 + q) : 0.0;
+      if (q0 == 0) acc = v[0];
+      else acc = __dadd_rn(acc, v[0]);
 #pragma unroll
       for (int q = 1; q < 16; ++q)
-        if (q < ns) acc = __dadd_rn(acc, v[q]);
-    } else {
-      acc = __ldcg(pr);
-      for (int q = 1; q < ns; ++q) acc = __dadd_rn(acc, __ldcg(pr + q));
+        if (q0 + q < ns) acc = __dadd_rn(acc, v[q]);
     }
     if (prm.xout)
       prm.xout[(int64_t)s * prm.xld + i] = acc;

@@ -202,3 +202,26 @@ def test_entropy_logits_and_trigger_bitwise_stats():
         assert stats[s, 0] == mean and stats[s, 1] == var  # bit-exact (NumPy order)
         assert bool(fire[s]) == ref.check_trigger(mean, var, 2.0, 0.5)
     assert st.gen_pages.cpu().tolist() == [1, 1, 1, 1]
+
+
+@pytest.mark.parametrize("vocab", [1, 7, 4099, 128256, 600000])
+def test_entropy_logits_vocab_sizes_and_masks(vocab):
+    """Entropy from logits at the Llama-3 vocabulary (and ragged / tiny /
+    over-sized vocabularies) with -inf-masked entries: |dH| <= 1e-4 nats
+    (SURVEY §8c), split count chosen by the kernel."""
+    rows = 5
+    g = torch.Generator(device="cuda").manual_seed(vocab)
+    logits = torch.randn(rows, vocab, device="cuda", generator=g) * torch.tensor(
+        [0.01, 1.0, 4.0, 20.0, 1.0], device="cuda").unsqueeze(1)
+    if vocab > 3:
+        logits[4, ::3] = -float("inf")  # masked vocabulary entries
+        logits[3, : vocab // 2] = -1e30
+    H = torch.zeros(rows, dtype=torch.float64, device="cuda")
+    nbytes = _lib.load().chess_entropy_workspace_bytes(rows)
+    ws = torch.zeros(nbytes, dtype=torch.uint8, device="cuda")
+    _lib.call("chess_entropy_logits", _lib.ptr(logits), rows, vocab, logits.stride(0), _lib.ptr(H),
+              _lib.ptr(ws), _lib.stream_ptr())
+    torch.cuda.synchronize()
+    for r in range(rows):
+        want = ref.entropy_from_logits(logits[r].double().cpu().numpy())
+        assert abs(H[r].item() - want) <= 1e-4, (r, H[r].item(), want)
