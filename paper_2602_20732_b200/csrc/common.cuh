@@ -445,6 +445,7 @@ __device__ void block_topk_mark(const uint64_t* keys, int n, int k, int* keep, i
   uint64_t mask = top_shift == 56 ? 0ull : ~0ull << (top_shift + 8);
   uint64_t prefix = gmax & mask;
   int kk = k;  // how many still to take among keys matching prefix
+  bool bin_taken = false;  // early exit: the k-th key's bin holds exactly kk keys
   for (int shift = top_shift; shift >= 0; shift -= 8) {
     for (int b = threadIdx.x; b < 256; b += NT) s_hist[b] = 0;
     block_sync<NT>();
@@ -493,14 +494,25 @@ __device__ void block_topk_mark(const uint64_t* keys, int n, int k, int* keep, i
         }
         s_scratch[0] = found_digit;
         s_scratch[1] = above;
+        s_scratch[2] = s_hist[found_digit];
       }
     }
     block_sync<NT>();
     const int digit = s_scratch[0];
     kk -= s_scratch[1];
+    const int in_bin = s_scratch[2];
     prefix |= ((uint64_t)digit) << shift;
     mask |= 0xFFull << shift;
     block_sync<NT>();
+    if (in_bin == kk) {  // every key of the bin is kept: no lower digits needed
+      bin_taken = true;
+      break;
+    }
+  }
+  if (bin_taken) {
+    for (int i = threadIdx.x; i < n; i += NT) keep[i] = (keys[i] & mask) >= prefix ? 1 : 0;
+    block_sync<NT>();
+    return;
   }
   // prefix == k-th largest key T; take all keys > T and the first kk keys == T.
   const uint64_t T = prefix;

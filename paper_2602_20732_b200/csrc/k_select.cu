@@ -747,13 +747,14 @@ __global__ void __launch_bounds__(kNT) prune_kernel(const double* s_g, int G, co
 }
 
 // masked top-k (selection.py:77-88 / oracle_flat_topk :114-123); one CTA.
+__device__ long long g_topk_trace[8];  // debug (trace build): phase cycles of the last topk_kernel
 __global__ void __launch_bounds__(kNT) topk_kernel(const double* scores, int n, int k,
                                                    const uint8_t* active, int32_t* out_idx,
                                                    int32_t* out_count, int sorted, uint8_t* wsb) {
   __shared__ TailSmem sm;
   uint64_t* keys = reinterpret_cast<uint64_t*>(wsb);
   int* kept = reinterpret_cast<int*>(wsb + 8 * (size_t)n);
-  int* cand = kept + n;
+  int* const cand = kept + n;
   int m = 0;
   for (int base = 0; base < n; base += kNT) {
     const int i = base + threadIdx.x;
@@ -764,9 +765,36 @@ __global__ void __launch_bounds__(kNT) topk_kernel(const double* scores, int n, 
     m += tot;
   }
   __syncthreads();
+  const long long tk0 = clock64();
+  if (m <= kTailCap) {  // keys and flags in shared memory, as in the scan tail
+    keys = sm.keys;
+    kept = sm.kept;
+  }
   for (int i = threadIdx.x; i < m; i += kNT) keys[i] = score_key(scores[cand[i]]);
   __syncthreads();
+  const long long tk1 = clock64();
   block_topk_mark<kNT>(keys, m, k, kept, sm.hist, sm.scratch);
+  const long long tk2 = clock64();
+  if (kTrace) {
+    // calibration: 64 named-barrier syncs, 64 bar.red.popc
+    const long long tb0 = clock64();
+    for (int i = 0; i < 64; ++i) block_sync<kNT>();
+    const long long tb1 = clock64();
+    int acc = 0;
+    for (int i = 0; i < 64; ++i) {
+      int c;
+      asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\tbar.red.popc.u32 %0, 1, %1, p;\n\t}"
+                   : "=r"(c) : "n"(kNT), "r"((int)((threadIdx.x + i) & 1)) : "memory");
+      acc += c;
+    }
+    const long long tb2 = clock64();
+    if (threadIdx.x == 0) {
+      g_topk_trace[0] = tk1 - tk0;
+      g_topk_trace[1] = tk2 - tk1;
+      g_topk_trace[2] = tb1 - tb0;
+      g_topk_trace[3] = tb2 - tb1 + (acc == -1);
+    }
+  }
   const int cnt = min(max(k, 0), m);
   if (sorted) {
     block_compact<kNT>(kept, m, out_idx, sm.scratch, [&](int i) { return cand[i]; });
@@ -942,6 +970,10 @@ int launch_build_ws_all(const ChessState& st, cudaStream_t stream) {
 }
 
 }  // namespace chess
+
+extern "C" int chess_debug_topk_trace(long long* host_out) {
+  return cudaMemcpyFromSymbol(host_out, chess::g_topk_trace, sizeof(chess::g_topk_trace)) == cudaSuccess ? 0 : 8;
+}
 
 extern "C" int chess_debug_select_trace(unsigned long long* host_out) {
   return cudaMemcpyFromSymbol(host_out, chess::g_sel_trace, sizeof(chess::g_sel_trace)) == cudaSuccess ? 0 : 8;
