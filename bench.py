@@ -117,7 +117,14 @@ def run_gpu(args):
 
     rank, world, local = _dist_env()
     torch.cuda.set_device(local)
-    if world > 1:
+    if world > 1 or args.shard == "head":
+        # (a 1-rank NCCL group for --shard head at N=1 exercises the real
+        # collectives inside the captured step graph)
+        if world == 1:
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", "29517")
+            os.environ.setdefault("RANK", "0")
+            os.environ.setdefault("WORLD_SIZE", "1")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     _lib.load()
     peaks = json.loads((REPO / "MEASURED_PEAKS.json").read_text()) if (REPO / "MEASURED_PEAKS.json").exists() else {}
@@ -434,7 +441,7 @@ def run_gpu(args):
         out["cpu_baseline"] = cpu_baseline(cfg_name, steps=1)
     if rank == 0:
         print(json.dumps(out), flush=True)
-    if world > 1:
+    if dist.is_initialized():
         dist.destroy_process_group()
 
 

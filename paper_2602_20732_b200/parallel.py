@@ -115,7 +115,7 @@ class HeadShardExchange:
         self._allgather = allgather or self._nccl_allgather
 
     def _nccl_allgather(self, out: torch.Tensor, inp: torch.Tensor) -> None:
-        if self.world == 1:
+        if self.world == 1 and not dist.is_initialized():
             if out.data_ptr() != inp.data_ptr():
                 out[0].copy_(inp)
             return
