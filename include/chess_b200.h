@@ -32,7 +32,7 @@
 extern "C" {
 #endif
 
-#define CHESS_ABI_VERSION 1
+#define CHESS_ABI_VERSION 2
 
 /* Status codes.  Python shim maps them to the pagesel exception classes
  * (pagesel/errors.py:4-21 and the ValueError/IndexError sites listed). */
@@ -134,6 +134,15 @@ typedef struct ChessState {
   int32_t* gen_pages;    /* [batch] generated pages completed                    */
   double* page_stats;    /* [batch][2] (mean_entropy, varentropy) of last page   */
   uint8_t* fire;         /* [batch] selection gate                               */
+  /* Optional device page pool: PagedKvStore's free list (kv_store.py:103-136)
+   * on the device, so generation never returns to the host for a page.
+   * pool_free == NULL: the caller fills page_table (host-managed).  A slot's
+   * pool pages are the run page_table[s][pool_base[s] .. pool_end[s]). */
+  int32_t* pool_free;    /* [n_phys] free physical page ids (a stack)            */
+  int32_t* pool_top;     /* [1] ids on the stack                                 */
+  int32_t* pool_base;    /* [batch] first page-table entry owned by the pool     */
+  int32_t* pool_end;     /* [batch] one past the last entry holding a pool page  */
+  uint8_t* pool_oom;     /* [batch] an allocation found the pool empty (sticky)  */
   void* workspace;
   size_t workspace_bytes;
 } ChessState;
@@ -208,6 +217,20 @@ int chess_summary_from_vectors(const ChessState* st, int32_t seq, const double* 
  * (hierarchy.py:102-136).  Used by the function-level HierarchyIndex API. */
 int chess_summary_fold(const ChessState* st, int32_t seq, const void* rows, int32_t dtype,
                        int32_t n_rows, int64_t row_stride, void* stream);
+
+/* ---- device page pool (kv_store.py:103-136: _allocate / OutOfPagesError) --
+ * chess_pool_init: the stack := ids[0..n) (device ids, n <= n_phys).
+ * chess_pool_reserve: slot s takes counts[s] pages (device i32 [batch]) into
+ *   page_table[s][pool_end ..) — all or none; none sets pool_oom[s].  Call it
+ *   with 1 at admission; afterwards chess_summary_seal reserves the next page
+ *   of every slot whose tail sealed, and chess_append_kv refuses to open a
+ *   page that was not reserved (pool_oom[s] = 1, the token is not written).
+ *   The caller maps a set pool_oom[s] to OutOfPagesError.
+ * chess_pool_release: slots with mask[s] (NULL: all) push their pool pages
+ *   back and clear pool_base/pool_end/pool_oom; call before chess_reset_slots. */
+int chess_pool_init(const ChessState* st, const int32_t* ids, int32_t n, void* stream);
+int chess_pool_reserve(const ChessState* st, const int32_t* counts, void* stream);
+int chess_pool_release(const ChessState* st, const uint8_t* mask, void* stream);
 
 /* K2+K3: anchor scoring + masked top-k cascade + working set + block table
  * (compute_anchor/score_all/hierarchical_prune/reconstruct_working_set/

@@ -21,7 +21,7 @@ from .errors import (
 )
 
 LIB_PATH = Path(__file__).resolve().parent / "libchess_b200.so"
-ABI_VERSION = 1
+ABI_VERSION = 2
 
 # enum ChessStatus
 OK, ERR_CONFIG, ERR_OUT_OF_PAGES, ERR_EMPTY_CONTEXT, ERR_SHAPE, ERR_INDEX, ERR_ORDER, ERR_VALUE, ERR_CUDA, ERR_UNSUPPORTED = range(10)
@@ -60,6 +60,7 @@ STATE_POINTERS = [
     "chunk_vec64", "grid_vec64", "page_vec32", "chunk_vec32", "grid_vec32", "key_sum",
     "anchor", "semantic", "n_semantic", "sel_stats", "ws_logical", "block_table",
     "ws_prov", "ws_len", "ent_ring", "ent_count", "gen_pages", "page_stats", "fire",
+    "pool_free", "pool_top", "pool_base", "pool_end", "pool_oom",
     "workspace",
 ]
 
@@ -112,6 +113,9 @@ SIGNATURES = {
     "chess_summary_from_vectors": (C.c_int, [C.POINTER(ChessState), _I32, _P, _I32, _I64, _P]),
     "chess_summary_fold": (C.c_int, [C.POINTER(ChessState), _I32, _P, _I32, _I32, _I64, _P]),
     "chess_select": (C.c_int, [C.POINTER(ChessState), C.POINTER(ChessSelectCfg), _P]),
+    "chess_pool_init": (C.c_int, [C.POINTER(ChessState), _P, _I32, _P]),
+    "chess_pool_reserve": (C.c_int, [C.POINTER(ChessState), _P, _P]),
+    "chess_pool_release": (C.c_int, [C.POINTER(ChessState), _P, _P]),
     "chess_select_partial": (C.c_int, [C.POINTER(ChessState), C.POINTER(ChessSelectCfg), _I32, _P, _I64, _P]),
     "chess_select_combine": (C.c_int, [C.POINTER(ChessState), C.POINTER(ChessSelectCfg), _I32, _P, _I32, _I64, _P]),
     "chess_build_working_set": (C.c_int, [C.POINTER(ChessState), _P]),

@@ -20,6 +20,9 @@ int launch_from_vectors(const ChessState&, int, const double*, int, int64_t, con
                         cudaStream_t);
 int launch_mean_rows(const void*, int, int64_t, int64_t, int64_t, double*, cudaStream_t);
 int launch_select(const ChessState&, const Workspace&, const SelParams&, int, cudaStream_t);
+int launch_pool_init(const ChessState&, const int32_t*, int, cudaStream_t);
+int launch_pool_reserve(const ChessState&, const int32_t*, cudaStream_t);
+int launch_pool_release(const ChessState&, const uint8_t*, cudaStream_t);
 int launch_select_partial(const ChessState&, const Workspace&, const SelParams&, int, cudaStream_t);
 int launch_select_combine(const ChessState&, const Workspace&, const SelParams&, int,
                           const double*, int, cudaStream_t);
@@ -330,6 +333,34 @@ int chess_select_combine(const ChessState* st, const ChessSelectCfg* cfg, int32_
   if (!gathered || world < 1) return fail(CHESS_ERR_SHAPE, "select_combine: bad gathered buffer / world");
   prm.xld = ld_partial;
   return launch_select_combine(*st, ws, prm, level, gathered, world, (cudaStream_t)stream);
+}
+
+static int pool_state(const ChessState* st) {
+  if (!st) return fail(CHESS_ERR_CONFIG, "null state");
+  if (!st->pool_free || !st->pool_top || !st->pool_base || !st->pool_end || !st->pool_oom)
+    return fail(CHESS_ERR_CONFIG, "state has no device page pool (pool_* pointers unset)");
+  return CHESS_OK;
+}
+
+int chess_pool_init(const ChessState* st, const int32_t* ids, int32_t n, void* stream) {
+  int rc = pool_state(st);
+  if (rc) return rc;
+  if (n < 0 || n > st->d.n_phys) return fail(CHESS_ERR_CONFIG, "pool of %d pages > n_phys %lld", n, (long long)st->d.n_phys);
+  if (n > 0 && !ids) return fail(CHESS_ERR_SHAPE, "pool_init: null ids");
+  return launch_pool_init(*st, ids, n, (cudaStream_t)stream);
+}
+
+int chess_pool_reserve(const ChessState* st, const int32_t* counts, void* stream) {
+  int rc = pool_state(st);
+  if (rc) return rc;
+  if (!counts) return fail(CHESS_ERR_SHAPE, "pool_reserve: null counts");
+  return launch_pool_reserve(*st, counts, (cudaStream_t)stream);
+}
+
+int chess_pool_release(const ChessState* st, const uint8_t* mask, void* stream) {
+  int rc = pool_state(st);
+  if (rc) return rc;
+  return launch_pool_release(*st, mask, (cudaStream_t)stream);
 }
 
 int chess_build_working_set(const ChessState* st, void* stream) {

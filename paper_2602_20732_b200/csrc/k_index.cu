@@ -11,6 +11,8 @@
 // reference's operation order, so the f64 state is bit-identical to pagesel's
 // given identical keys.  The f32 matrices are rounded mirrors used only by the
 // selection scan.
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace chess {
@@ -78,6 +80,73 @@ __device__ __forceinline__ FoldOut fold_page(double v, int p, int Nc, int Ng, do
 // ---------------------------------------------------------------------------
 // reset
 // ---------------------------------------------------------------------------
+// ---------------------------------------------------------------------------
+// device page pool (kv_store.py:103-136): a stack of free physical ids.
+// ---------------------------------------------------------------------------
+// Slot s takes `cnt` pages into page_table[s][pool_end ..), all or none (CAS
+// loop on the stack top: no spurious failure under contention).  One thread.
+__device__ bool pool_take(const ChessState& st, int s, int cnt) {
+  const ChessDims& d = st.d;
+  int end = st.pool_end[s];
+  const int np = st.num_pages[s];
+  if (end < np) {  // entries before num_pages were filled by the caller
+    st.pool_base[s] = np;
+    end = np;
+  }
+  if (cnt <= 0) return true;
+  if (end + cnt > d.max_pages) {
+    st.pool_oom[s] = 1;
+    return false;
+  }
+  int top = atomicAdd(st.pool_top, 0);
+  for (;;) {
+    if (top < cnt) {
+      st.pool_oom[s] = 1;
+      return false;
+    }
+    const int seen = atomicCAS(st.pool_top, top, top - cnt);
+    if (seen == top) break;
+    top = seen;
+  }
+  int32_t* row = st.page_table + (int64_t)s * d.max_pages;
+  for (int i = 0; i < cnt; ++i) row[end + i] = st.pool_free[top - 1 - i];
+  st.pool_end[s] = end + cnt;
+  return true;
+}
+
+__global__ void pool_init_kernel(ChessState st, const int32_t* ids, int n) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    st.pool_free[i] = ids[i];
+  if (blockIdx.x == 0 && threadIdx.x == 0) *st.pool_top = n;
+}
+
+__global__ void pool_reserve_kernel(ChessState st, const int32_t* counts) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= st.d.batch) return;
+  pool_take(st, s, counts[s]);
+}
+
+// one CTA per slot: push the slot's pool pages back
+__global__ void pool_release_kernel(ChessState st, const uint8_t* mask) {
+  __shared__ int s_pos;
+  const int s = blockIdx.x;
+  if (mask && !mask[s]) return;
+  const int base = st.pool_base[s], end = st.pool_end[s];
+  const int n = end - base;
+  if (n > 0) {
+    if (threadIdx.x == 0) s_pos = atomicAdd(st.pool_top, n);
+    __syncthreads();
+    const int32_t* row = st.page_table + (int64_t)s * st.d.max_pages;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) st.pool_free[s_pos + i] = row[base + i];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    st.pool_base[s] = 0;
+    st.pool_end[s] = 0;
+    st.pool_oom[s] = 0;
+  }
+}
+
 __global__ void reset_kernel(ChessState st, const uint8_t* mask) {
   const int s = blockIdx.x;
   if (mask && !mask[s]) return;
@@ -121,6 +190,11 @@ __global__ void __launch_bounds__(kNT) append_kernel(ChessState st, const __nv_b
   const int np = st.num_pages[s];
   const int fill = st.tail_fill[s];
   const bool open_new = (np == 0) || (fill >= B);
+  if (st.pool_free && open_new && st.pool_end[s] <= np) {
+    // device pool: the page this token opens was never reserved (pool empty)
+    if (blockIdx.x == 0 && threadIdx.x == 0) st.pool_oom[s] = 1;
+    return;
+  }
   const int slot = open_new ? np : np - 1;
   const int row = open_new ? 0 : fill;
   const int64_t phys = st.page_table[(int64_t)s * d.max_pages + slot];
@@ -231,6 +305,8 @@ __global__ void __launch_bounds__(kNT) seal_kernel(ChessState st, int32_t* done)
     done[s] = 0;
     st.num_sealed[s] = P + 1;
     st.sealed[s] = 0;
+    // device pool: the slot's next append opens page num_pages — reserve it now
+    if (st.pool_free && st.pool_end[s] <= st.num_pages[s]) pool_take(st, s, 1);
   }
 }
 
@@ -499,6 +575,21 @@ __global__ void mean_rows_kernel(const T* rows, int64_t n, int64_t dim, int64_t 
 int launch_reset(const ChessState& st, const uint8_t* mask, cudaStream_t stream) {
   reset_kernel<<<st.d.batch, 256, 0, stream>>>(st, mask);
   return check_launch("reset_slots");
+}
+
+int launch_pool_init(const ChessState& st, const int32_t* ids, int n, cudaStream_t stream) {
+  pool_init_kernel<<<std::max(1, std::min(148, (n + 255) / 256)), 256, 0, stream>>>(st, ids, n);
+  return check_launch("pool_init");
+}
+
+int launch_pool_reserve(const ChessState& st, const int32_t* counts, cudaStream_t stream) {
+  pool_reserve_kernel<<<(st.d.batch + 127) / 128, 128, 0, stream>>>(st, counts);
+  return check_launch("pool_reserve");
+}
+
+int launch_pool_release(const ChessState& st, const uint8_t* mask, cudaStream_t stream) {
+  pool_release_kernel<<<st.d.batch, 128, 0, stream>>>(st, mask);
+  return check_launch("pool_release");
 }
 
 int launch_append(const ChessState& st, const Workspace& ws, const void* k_rows, const void* v_rows,

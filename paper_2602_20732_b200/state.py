@@ -56,7 +56,7 @@ class Shape:
 class DecodeState:
     """Allocates and owns every buffer of a ChessState for `shape`."""
 
-    def __init__(self, shape: Shape, device="cuda", kv_pool=None):
+    def __init__(self, shape: Shape, device="cuda", kv_pool=None, page_pool=False):
         self.shape = s = shape
         self.device = torch.device(device)
         dev = self.device
@@ -103,6 +103,15 @@ class DecodeState:
         self.gen_pages = torch.zeros(b, **i32)
         self.page_stats = torch.zeros((b, 2), **f64)
         self.fire = torch.zeros(b, **u8)
+        # optional device page pool (kv_store.py:103-136 free list on the device)
+        if page_pool:
+            self.pool_free = torch.zeros(s.n_phys, **i32)
+            self.pool_top = torch.zeros(1, **i32)
+            self.pool_base = torch.zeros(b, **i32)
+            self.pool_end = torch.zeros(b, **i32)
+            self.pool_oom = torch.zeros(b, **u8)
+        else:
+            self.pool_free = self.pool_top = self.pool_base = self.pool_end = self.pool_oom = None
 
         self.c = _lib.ChessState()
         d = self.c.d
@@ -124,6 +133,40 @@ class DecodeState:
     # ------------------------------------------------------------------
     def reset(self, mask=None, stream=None):
         _lib.call("chess_reset_slots", self.ref, _lib.ptr(mask), _lib.stream_ptr(stream))
+
+    # ------------------------------------------------------------------
+    # device page pool
+    # ------------------------------------------------------------------
+    def pool_init(self, ids=None, stream=None):
+        """Free list := ids (default: every physical page), kv_store.py:117-120."""
+        if ids is None:
+            ids = torch.arange(self.shape.n_phys, dtype=torch.int32, device=self.device)
+        ids = torch.as_tensor(ids, dtype=torch.int32, device=self.device).contiguous()
+        self._pool_ids = ids  # kept alive until the (async) copy ran
+        _lib.call("chess_pool_init", self.ref, _lib.ptr(ids), int(ids.numel()), _lib.stream_ptr(stream))
+
+    def pool_reserve(self, counts, stream=None):
+        """Slot s takes counts[s] pages into its page table (admission)."""
+        c = torch.as_tensor(counts, dtype=torch.int32, device=self.device).reshape(-1)
+        if c.numel() == 1 and self.shape.batch > 1:
+            c = c.expand(self.shape.batch)
+        c = c.contiguous()
+        self._pool_counts = c
+        _lib.call("chess_pool_reserve", self.ref, _lib.ptr(c), _lib.stream_ptr(stream))
+
+    def pool_release(self, mask=None, stream=None):
+        _lib.call("chess_pool_release", self.ref, _lib.ptr(mask), _lib.stream_ptr(stream))
+
+    def pool_free_count(self) -> int:
+        return int(self.pool_top.item())
+
+    def check_pool(self):
+        """Raise OutOfPagesError (kv_store.py:129-132) if an allocation failed."""
+        from .errors import OutOfPagesError
+
+        if self.pool_oom is not None and bool(self.pool_oom.any()):
+            slots = torch.nonzero(self.pool_oom).flatten().tolist()
+            raise OutOfPagesError(f"device page pool exhausted ({self.shape.n_phys} pages); slots {slots}")
 
     def scan_matrices(self):
         """(grid, chunk, page) matrices the selection scan reads."""
