@@ -43,13 +43,19 @@ def _stale(target: Path, deps) -> bool:
     return any(Path(d).stat().st_mtime > t for d in deps)
 
 
-def build(verbose: bool = False, force: bool = False, trace: bool = False) -> Path:
+def build(verbose: bool = False, force: bool = False, trace: bool = False, variant: str = "",
+          defines=()) -> Path:
     """Product library; trace=True builds the debug-timeline variant
     (-DCHESS_TRACE=1) as libchess_b200_trace.so for the micro-benchmarks
-    (select it with CHESS_B200_LIB)."""
+    (select it with CHESS_B200_LIB).  variant/defines build an experiment
+    library libchess_b200_<variant>.so with extra -D flags."""
     bdir = BUILD / "trace" if trace else BUILD
     lib = TRACE_LIB if trace else LIB
     extra = ["-DCHESS_TRACE=1"] if trace else []
+    if variant:
+        bdir = BUILD / variant
+        lib = PKG_DIR / f"libchess_b200_{variant}.so"
+        extra += [f"-D{x}" for x in defines]
     bdir.mkdir(parents=True, exist_ok=True)
     objs = []
     for src in SOURCES:
@@ -78,4 +84,6 @@ def build(verbose: bool = False, force: bool = False, trace: bool = False) -> Pa
 
 
 if __name__ == "__main__":
-    build(verbose=True, force="--force" in sys.argv, trace="--trace" in sys.argv)
+    var = next((a.split("=", 1)[1] for a in sys.argv if a.startswith("--variant=")), "")
+    defs = [a.split("=", 1)[1] for a in sys.argv if a.startswith("--define=")]
+    build(verbose=True, force="--force" in sys.argv, trace="--trace" in sys.argv, variant=var, defines=defs)

@@ -76,7 +76,7 @@ struct Workspace {
 };
 
 constexpr int kEntSplit = 64;  // max CTAs per logit row (entropy split partials)
-constexpr int kAttnCtasMax = 160;               // attention CTAs (<= SMs)
+constexpr int kAttnCtasMax = 320;               // attention CTAs (<= 2 per SM)
 constexpr int kAttnWarpsMax = kAttnCtasMax * 8; // stream-K warps (partial slots)
 
 size_t workspace_layout(const ChessDims& d, void* base, Workspace* ws);

@@ -26,6 +26,7 @@
 //    it (atomic counter), in CTA order — deterministic.
 #include <cudaTypedefs.h>
 
+#include <algorithm>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -34,24 +35,26 @@ namespace chess {
 
 namespace {
 
-// Consumer warps per CTA and CTAs per SM (build-time knobs).  Measured on
-// B200, cfg3 layer (tools/attn_micro.py, graph-replayed): 4 consumers x 1 CTA
-// (13-stage ring) 19.1 us; 8 x 1: 19.8 us; 6 x 2: 28.1 us; 8 x 2: 34.4 us --
-// two co-resident CTAs halve each ring and the layers fight for HBM.
+// Consumer warps per CTA (build-time knob) and CTAs per SM (CPS, a template
+// parameter chosen per launch).  Measured on B200 (tools/attn_micro.py,
+// graph-replayed, profiles/r01/attn_micro/): 4 consumers x 1 CTA (13-stage
+// ring) 19.1 us at cfg3 vs 19.8 with 8 consumers.  Two co-resident CTAs per
+// SM (6-stage rings) lose when segments <= SMs (cfg3 19.6 us, cfg5 17.5 vs
+// 14.5) but win in the stream-K regime (batch x kv_heads > SMs: cfg4 48.3 vs
+// 51.2 us, b=32 32.6 vs 36.4): layer l+1's CTAs start in the freed half of
+// each SM while layer l drains.
 #ifndef CHESS_ATTN_CONSUMERS
 #define CHESS_ATTN_CONSUMERS 4
 #endif
-#ifndef CHESS_ATTN_CTAS_PER_SM
-#define CHESS_ATTN_CTAS_PER_SM 1
-#endif
 constexpr int kConsumers = CHESS_ATTN_CONSUMERS;
-constexpr int kCtasPerSm = CHESS_ATTN_CTAS_PER_SM;
+constexpr int kMaxCtasPerSm = 2;
 constexpr int kAttnMaxBatch = 256;  // per-slot tables live in smem
 constexpr int kMinPiece = 4;  // piece mode: pages per piece >= 4 (bounds the merge fan-in)
 constexpr int kThreads = (kConsumers + 1) * 32;
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kLn2 = 0.6931471805599453f;
-constexpr int kSmemBudget = (228 * 1024) / kCtasPerSm - 1024 - 256;  // minus reserved + static smem
+// per-CTA dynamic smem budget at CPS CTAs per SM, minus reserved + static smem
+__host__ __device__ constexpr int smem_budget(int cps) { return (228 * 1024) / cps - 1024 - 256; }
 
 struct AttnArgs {
   const __nv_bfloat16* q;
@@ -81,11 +84,11 @@ __device__ __forceinline__ void trace_max(int which) {
   if (kTrace) atomicMax(&s_trace[which], (unsigned long long)global_ns());
 }
 
-constexpr int kMaxCluster = 8;  // portable cluster size
+constexpr int kMaxCluster = 8;  // portable cluster size cap (inbox slots = cap - 1)
 
 // XC: cluster-merge variant (piece mode with one segment per thread-block
 // cluster): the leader CTA owns an inbox for the other CTAs' piece states.
-template <int HD, int GQ, int B, bool XC = false>
+template <int HD, int GQ, int B, bool XC = false, int CPS = 1>
 struct Cfg {
   static constexpr int kCB = HD / 64;                  // 128-byte column blocks
   static constexpr int kPageBytes = B * HD * 2;        // K (or V) bytes of a page
@@ -98,7 +101,7 @@ struct Cfg {
   static constexpr int kXBytes = XC ? (kMaxCluster - 1) * GQ * kRow * 4 : 0;  // leader's inbox
   static constexpr int kMisc = kTables + 64 * 8 + 64 + 1024;  // tables, barriers, counters, align
   static constexpr int kStagesRaw =
-      (kSmemBudget - kStateBytes - kQSlots * kQBytes - kXBytes - kMisc) / kStageBytes;
+      (smem_budget(CPS) - kStateBytes - kQSlots * kQBytes - kXBytes - kMisc) / kStageBytes;
   static constexpr int kStages = kStagesRaw > 32 ? 32 : kStagesRaw;
   static constexpr int kMT = B / 16;                   // QK m-tiles (16 tokens each)
   static constexpr int kKS = HD / 16;                  // QK k-steps over d
@@ -222,12 +225,12 @@ __device__ __forceinline__ void st_release_cta(int* p, int v) {
 // arrives on the leader's mbarrier (release.cluster); the leader merges the
 // states in cluster-rank order.  This replaces the split-segment path's
 // global partials + fences + atomics (~3 us of round trips) on small batches.
-template <int HD, int GQ, int B, bool XC>
-__global__ void __launch_bounds__(kThreads, kCtasPerSm)
+template <int HD, int GQ, int B, bool XC, int CPS>
+__global__ void __launch_bounds__(kThreads, CPS)
     sparse_decode_kernel(ChessState st, Workspace ws, AttnArgs args,
                          const __grid_constant__ CUtensorMap kmap,
                          const __grid_constant__ CUtensorMap vmap) {
-  using C = Cfg<HD, GQ, B, XC>;
+  using C = Cfg<HD, GQ, B, XC, CPS>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* ring = smem;
@@ -893,7 +896,7 @@ template <int HD, int GQ, int B>
 int launch_cluster(const ChessState& st, const Workspace& ws, const AttnArgs& args, int segs,
                    cudaStream_t stream) {
   using C = Cfg<HD, GQ, B, true>;
-  auto kfn = sparse_decode_kernel<HD, GQ, B, true>;  // smem attribute set by cluster_size_for
+  auto kfn = sparse_decode_kernel<HD, GQ, B, true, 1>;  // smem attribute set by cluster_size_for
   CUtensorMap km, vm;
   int rc = make_kv_map(&km, st.k_pool, st.d);
   if (rc) return rc;
@@ -927,7 +930,7 @@ template <int HD, int GQ, int B>
 int cluster_size_for(int segs) {
   static int max_active[kMaxCluster + 1] = {};
   static bool probed = false;
-  auto kfn = sparse_decode_kernel<HD, GQ, B, true>;
+  auto kfn = sparse_decode_kernel<HD, GQ, B, true, 1>;
   using C = Cfg<HD, GQ, B, true>;
   if (!probed) {
     cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::kSmem);
@@ -959,6 +962,10 @@ int cluster_size_for(int segs) {
   return 0;
 }
 
+template <int HD, int GQ, int B, int CPS>
+int launch_grid(const ChessState& st, const Workspace& ws, const AttnArgs& args, int nctas,
+                cudaStream_t stream);
+
 template <int HD, int GQ, int B>
 int launch_inst(const ChessState& st, const Workspace& ws, const AttnArgs& args_in, int nctas,
                 cudaStream_t stream) {
@@ -966,10 +973,20 @@ int launch_inst(const ChessState& st, const Workspace& ws, const AttnArgs& args_
   const int segs = st.d.batch * st.d.kv_heads;
   args.cl = args.mode == 7 ? 0 : cluster_size_for<HD, GQ, B>(segs);
   if (args.cl) return launch_cluster<HD, GQ, B>(st, ws, args, segs, stream);
-  using C = Cfg<HD, GQ, B>;
+  // stream-K regime: two CTAs per SM over half-depth rings
+  static const int cps_env = getenv("CHESS_ATTN_CPS") ? atoi(getenv("CHESS_ATTN_CPS")) : 0;  // A/B
+  const int cps = cps_env ? cps_env : (segs > num_sms() ? 2 : 1);
+  if (cps == 2) return launch_grid<HD, GQ, B, 2>(st, ws, args, std::min(nctas, 2 * num_sms()), stream);
+  return launch_grid<HD, GQ, B, 1>(st, ws, args, std::min(nctas, num_sms()), stream);
+}
+
+template <int HD, int GQ, int B, int CPS>
+int launch_grid(const ChessState& st, const Workspace& ws, const AttnArgs& args, int nctas,
+                cudaStream_t stream) {
+  using C = Cfg<HD, GQ, B, false, CPS>;
   const size_t smem = C::kSmem;
   static bool configured = false;
-  auto kfn = sparse_decode_kernel<HD, GQ, B, false>;
+  auto kfn = sparse_decode_kernel<HD, GQ, B, false, CPS>;
   if (!configured) {
     cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     configured = true;
@@ -998,7 +1015,7 @@ int launch_inst(const ChessState& st, const Workspace& ws, const AttnArgs& args_
 
 int attn_ctas_for(const ChessDims& d) {
   (void)d;
-  return num_sms();
+  return kMaxCtasPerSm * num_sms();
 }
 
 int launch_sparse_decode(const ChessState& st, const Workspace& ws, int layer, const void* q,

@@ -188,3 +188,40 @@ def test_attention_restatement_vs_dense():
             w = np.exp(z) / np.exp(z).sum()
             np.testing.assert_allclose(o[s, h], w @ Vs[h // 2], rtol=1e-12, atol=1e-12)
             np.testing.assert_allclose(lse[s, h], np.log(np.exp(z).sum()), rtol=1e-12)
+
+
+def test_attention_bf16_bound_covers_kernel_rounding():
+    """oracle/attention.bf16_bound holds for an emulation of K4's rounding
+    (fp32 scores and exp, P rounded to bf16 for the PV product, fp32 l from
+    unrounded p, bf16 output) — including one-page working sets."""
+    import torch
+
+    from oracle import attention as attn
+
+    rng = np.random.default_rng(3)
+    bf = lambda x: torch.as_tensor(x, dtype=torch.float32).to(torch.bfloat16).double().numpy()
+    worst = 0.0
+    for trial in range(40):
+        B, d, hkv, grp = 32, 64, 2, 4
+        n_phys = 12
+        ws = int(rng.integers(1, 5))
+        fill = int(rng.integers(1, B + 1))
+        kp = bf(rng.standard_normal((n_phys, hkv, B, d)) * rng.choice([0.5, 1.0, 3.0]))
+        vp = bf(rng.standard_normal((n_phys, hkv, B, d)))
+        q = bf(rng.standard_normal((1, hkv * grp, d)))
+        bt = [rng.choice(n_phys, size=ws, replace=False)]
+        scale = 1.0 / np.sqrt(d)
+        o_ref, _ = attn.sparse_decode(q, kp, vp, bt, [ws], [fill], scale)
+        tol = attn.bf16_bound(q, kp, vp, bt, [ws], [fill], scale, o_ref)
+        for h in range(hkv):
+            K = attn.gather_tokens(kp, bt[0], ws, fill, h).astype(np.float32)
+            V = attn.gather_tokens(vp, bt[0], ws, fill, h).astype(np.float32)
+            for g in range(grp):
+                qh = h * grp + g
+                z = (K @ q[0, qh].astype(np.float32)) * np.float32(scale)
+                p = np.exp(z - z.max()).astype(np.float32)
+                o = (bf(p).astype(np.float32) @ V) / p.sum(dtype=np.float32)
+                err = np.abs(bf(o) - o_ref[0, qh])
+                assert np.all(err <= tol[0, qh]), (trial, (err / tol[0, qh]).max())
+                worst = max(worst, float((err / tol[0, qh]).max()))
+    assert worst > 0.05  # the bound is not vacuous
