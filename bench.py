@@ -116,8 +116,16 @@ def run_gpu(args):
     from paper_2602_20732_b200.synthetic import CONFIGS, DESCRIPTIONS, SyntheticDecode
 
     rank, world, local = _dist_env()
+    # CHESS_BENCH_ONE_DEVICE=1 (plumbing test only): every rank on cuda:0 over
+    # gloo, so the multi-rank paths (barriers, max-over-ranks, rank-0 output)
+    # run on a 1-GPU box; never used for a reported number
+    one_dev = os.environ.get("CHESS_BENCH_ONE_DEVICE") == "1"
+    if one_dev:
+        local = 0
     torch.cuda.set_device(local)
-    if world > 1 or args.shard == "head":
+    if one_dev and world > 1:
+        dist.init_process_group("gloo")
+    elif world > 1 or args.shard == "head":
         # (a 1-rank NCCL group for --shard head at N=1 exercises the real
         # collectives inside the captured step graph)
         if world == 1:
@@ -146,7 +154,8 @@ def run_gpu(args):
     ring = 64 if c["page"] == 32 else 32
     gen_pages = math.ceil((total_steps + 2 * ring + 64) / c["page"]) + 4
     wl = SyntheticDecode(cfg_name, batch=batch, gen_pages=gen_pages, ring=ring, seed=rank,
-                         summary_dtype=args.summary_dtype, head_shard=(rank, world) if head else None)
+                         summary_dtype=args.summary_dtype, head_shard=(rank, world) if head else None,
+                         kv_budget_gib=args.kv_gib)
     st = wl.st
     sh = wl.shape
     sel = preset_config("aggressive", page_size=sh.page_size)
@@ -482,16 +491,27 @@ def _cpu_step(ref, cfg, h, k_pool, v_pool, q, logits, dims):
     return len(pages)
 
 
+def _all_host_threads():
+    """BLAS thread pools sized to every host core (torchrun exports
+    OMP_NUM_THREADS=1, which would otherwise pin the CPU arm to one thread)."""
+    from threadpoolctl import threadpool_limits
+
+    n = os.cpu_count() or 1
+    return threadpool_limits(limits=n), n
+
+
 def cpu_baseline(cfg_name, steps=1):
     setup = _cpu_sample_setup(cfg_name)
-    t = time.perf_counter()
-    for _ in range(steps):
-        _cpu_step(*setup)
-    dt = (time.perf_counter() - t) / steps
+    limits, cores = _all_host_threads()
+    with limits:
+        t = time.perf_counter()
+        for _ in range(steps):
+            _cpu_step(*setup)
+        dt = (time.perf_counter() - t) / steps
     return {
         "value": 1.0 / dt,
         "unit": "tokens/s",
-        "cores": os.cpu_count(),
+        "cores": cores,
         "kind": "port",
         "sample": f"1 sequence x 1 decode step of {cfg_name} (selection over the full index + "
                   f"{setup[-1][0]}-layer attention restatement + entropy), oracle/ NumPy port, "
@@ -507,12 +527,14 @@ def run_reference(args):
     from paper_2602_20732_b200.synthetic import DESCRIPTIONS
 
     setup = _cpu_sample_setup(args.config)
-    for _ in range(min(args.warmup, 1)):
-        _cpu_step(*setup)
-    t = time.perf_counter()
-    for _ in range(args.steps):
-        _cpu_step(*setup)
-    dt = (time.perf_counter() - t) / args.steps
+    limits, cores = _all_host_threads()
+    with limits:
+        for _ in range(min(args.warmup, 1)):
+            _cpu_step(*setup)
+        t = time.perf_counter()
+        for _ in range(args.steps):
+            _cpu_step(*setup)
+        dt = (time.perf_counter() - t) / args.steps
     v = 1.0 / dt
     sample = (f"each step = 1 sequence x 1 decode token of {args.config} (oracle NumPy port of "
               f"pagesel selection + attention restatement + entropy)")
@@ -523,7 +545,7 @@ def run_reference(args):
         "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"{args.config}: {DESCRIPTIONS[args.config]}"},
-        "cpu_baseline": {"value": v, "unit": "tokens/s", "cores": os.cpu_count(), "kind": "port",
+        "cpu_baseline": {"value": v, "unit": "tokens/s", "cores": cores, "kind": "port",
                          "sample": sample},
         "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
@@ -541,6 +563,8 @@ def main():
     ap.add_argument("--full-scan", action="store_true")
     ap.add_argument("--headline-only", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--kv-gib", type=float, default=None,
+                    help="KV pool budget per GPU (default: all free HBM minus headroom)")
     ap.add_argument("--shard", default="auto", choices=["auto", "batch", "head", "replica"],
                     help="multi-GPU partitioning (auto: cfg4 batch, cfg5 kv-head, else replicas)")
     args = ap.parse_args()
