@@ -14,3 +14,6 @@ timeout 600 ncu --set full --clock-control none --import-source on -k regex:spar
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:select_scan -s 12 -c 3 \
   -o $OUT/select python bench.py --steps 3 --warmup 3 --headline-only --no-cpu-baseline > $OUT/select.log 2>&1
 ls -la $OUT
+timeout 600 ncu --set full --clock-control none --import-source on -k 'regex:entropy_kernel|append_kernel|seal_kernel' -s 30 -c 3 \
+  -o $OUT/small python bench.py --steps 3 --warmup 3 --headline-only --no-cpu-baseline > $OUT/small.log 2>&1
+ls -la $OUT
