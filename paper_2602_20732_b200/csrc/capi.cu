@@ -105,6 +105,7 @@ size_t workspace_layout(const ChessDims& d, void* base, Workspace* ws) {
     return o;
   };
   const size_t o_sel_done = take(b * 4);
+  const size_t o_flow = take((1 + 4 * b) * 4);
   const size_t o_cand = take(b * 3 * mr * 4);
   const size_t o_cand_n = take(b * 4 * 4);
   const size_t o_scores = take(b * mr * 8);
@@ -121,6 +122,7 @@ size_t workspace_layout(const ChessDims& d, void* base, Workspace* ws) {
   if (ws && base) {
     uint8_t* p = reinterpret_cast<uint8_t*>(base);
     ws->sel_done = reinterpret_cast<int32_t*>(p + o_sel_done);
+    ws->flow = reinterpret_cast<int32_t*>(p + o_flow);
     ws->cand = reinterpret_cast<int32_t*>(p + o_cand);
     ws->cand_n = reinterpret_cast<int32_t*>(p + o_cand_n);
     ws->scores = reinterpret_cast<double*>(p + o_scores);

@@ -58,6 +58,8 @@ constexpr bool kTrace = CHESS_TRACE != 0;
 
 struct Workspace {
   int32_t* sel_done;     // [batch]
+  int32_t* flow;         // select dataflow scheduler: [0] next item, [1 .. 3b] items done per
+                         // (level, slot), [1+3b .. 1+4b] levels finished per slot
   int32_t* cand;         // [batch][3][max_rows]  candidate row ids per level
   int32_t* cand_n;       // [batch][4]            candidate counts (levels 0..2, full)
   double* scores;        // [batch][max_rows]     reduced scores of the current level
@@ -310,6 +312,14 @@ __device__ __forceinline__ void tma_load_1d(void* dst_smem, const void* src_gmem
 // cheaper than __threadfence() (fence.sc.gpu + L1 invalidate, SASS ERRBAR +
 // CCTL.IVALL), which showed up as microseconds per split-K merge.
 __device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+__device__ __forceinline__ int ld_acquire_gpu(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_gpu(int* p, int v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 
 // explicit shared-window vector loads (a generic pointer into dynamic smem
 // after alignment arithmetic compiles to LD.E, not LDS)

@@ -74,7 +74,7 @@ __device__ __forceinline__ const float* level_row_ptr<float>(const ChessState& s
     row = which == 0 ? i : (which == 1 ? i - sh.G : i - sh.G - sh.C);
   } else {
     which = level;
-    row = level == 0 ? i : ws.cand[((int64_t)s * 3 + level) * mr + i];
+    row = level == 0 ? i : __ldcg(&ws.cand[((int64_t)s * 3 + level) * mr + i]);  // may be this launch's
   }
   if (which == 0) return st.grid_vec32 + ((int64_t)s * max_grids(d) + row) * d.ld;
   if (which == 1) return st.chunk_vec32 + ((int64_t)s * max_chunks(d) + row) * d.ld;
@@ -94,7 +94,7 @@ __device__ __forceinline__ const double* level_row_ptr<double>(const ChessState&
     row = which == 0 ? i : (which == 1 ? i - sh.G : i - sh.G - sh.C);
   } else {
     which = level;
-    row = level == 0 ? i : ws.cand[((int64_t)s * 3 + level) * mr + i];
+    row = level == 0 ? i : __ldcg(&ws.cand[((int64_t)s * 3 + level) * mr + i]);  // may be this launch's
   }
   if (which == 0) return st.grid_vec64 + ((int64_t)s * max_grids(d) + row) * d.ld;
   if (which == 1) return st.chunk_vec64 + ((int64_t)s * max_chunks(d) + row) * d.ld;
@@ -626,6 +626,387 @@ __global__ void __launch_bounds__(kScanCTA, 1) select_scan_kernel(ChessState st,
 }
 
 // ---------------------------------------------------------------------------
+// Dataflow cascade (conditional scan, one launch for all three levels).
+//
+// Items are (level, slot, slice, row block) in level-major, slot-minor order;
+// each (level, slot) gets an UPPER BOUND of row blocks known at launch
+// (level 1 <= k_g*N_g children, level 2 <= ceil(rho_c*that)*N_c), so the item
+// space is static while the actual candidate counts are produced by the
+// tails.  CTAs grab items from a global counter; an item of level l >= 1 of
+// slot s waits (producer side) until slot s's level l-1 tail has published
+// its candidates (flow_lvl[s] >= l, release/acquire at gpu scope).  Rows past
+// the actual count make an item empty; every item, empty or not, counts
+// towards its (level, slot) completion and the CTA that completes it runs the
+// tail (same select_tail as the per-level kernel).  Level l+1 of early slots
+// therefore streams while later slots are still finishing level l, and there
+// is one launch/prologue instead of three.  Measured slower than the
+// per-level kernel so far (see launch_select); opt-in with CHESS_SELECT_FLOW=1.
+//
+// Completions are counted per (CTA, level, slot) run and flushed when the
+// next descriptor belongs to another (level, slot), at the end, or when the
+// producer is about to block on a dependency (a FLUSH descriptor) — so a
+// CTA never sits on the last contribution a tail it waits for needs.
+// Deadlock freedom: items are grabbed in level order and a tail depends only
+// on items of its own level, which never wait on later levels.
+// ---------------------------------------------------------------------------
+constexpr int kDescRing = 8;
+constexpr int kFlowMaxBatch = 256;  // per-slot scheduler tables live in shared memory
+constexpr int kDescEnd = -1, kDescFlush = -2;
+struct FlowDesc {
+  int s, level, r0, rows, slice;  // rows: >= 0 item rows, kDescEnd, kDescFlush
+};
+
+__device__ __forceinline__ int flow_row_bound(const ChessState& st, const SelParams& prm, int s,
+                                              int level) {
+  if (!fired(st, prm, s)) return 0;
+  const LevelShape sh = shape_of(st, s);
+  if (sh.P == 0) return 0;
+  if (level == 0) return sh.G;
+  // ceil in double, as the tail's k (selection.py:98, 103)
+  const int kg = (int)ceil(prm.rho[0] * (double)sh.G);
+  const int r1 = min(sh.C, kg * st.d.chunks_per_grid);
+  if (level == 1) return r1;
+  const int kc = (int)ceil(prm.rho[1] * (double)r1);
+  return min(sh.P, kc * st.d.pages_per_chunk);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kScanCTA, 1) select_flow_kernel(ChessState st, Workspace ws,
+                                                                  SelParams prm) {
+  using SC = ScanCfg<T>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* ring = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
+  uint64_t* full = reinterpret_cast<uint64_t*>(ring + (size_t)SC::kStages * SC::kStageBytes);
+  uint64_t* empty = full + SC::kStages;
+  uint64_t* dfull = empty + SC::kStages;
+  uint64_t* dempty = dfull + kDescRing;
+  FlowDesc* desc = reinterpret_cast<FlowDesc*>(dempty + kDescRing);
+  int* s_pre = reinterpret_cast<int*>(desc + kDescRing);  // [3 * batch + 1]
+  int* s_ready = s_pre + 3 * st.d.batch + 1;               // [batch] levels seen published (producer)
+  int* s_nrb = s_ready + st.d.batch;                       // [3][batch] row blocks (upper bound)
+  int* s_n = s_nrb + 3 * st.d.batch;                       // [3][batch] actual rows (once published)
+  __shared__ double s_wpart[2][kScanRows][kWarps];
+  __shared__ TailSmem sm;
+  __shared__ int s_last;
+  const ChessDims& d = st.d;
+  const int nb = d.batch;
+  const int nsl = ws.n_slices;
+  const int64_t mr = max_rows(d);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int* next = ws.flow;
+  int* done = ws.flow + 1;           // [3][batch]
+  int* lvl = ws.flow + 1 + 3 * nb;   // [batch]
+
+  // item prefix over (level, slot): upper-bound row blocks x slices
+  if (warp == 0) {
+    int run = 0;
+    for (int l = 0; l < 3; ++l) {
+      for (int b0 = 0; b0 < nb; b0 += 32) {
+        const int s = b0 + lane;
+        const int nrb = s < nb ? (flow_row_bound(st, prm, s, l) + kScanRows - 1) / kScanRows : 0;
+        const int items = nrb * nsl;
+        if (s < nb) {
+          s_nrb[l * nb + s] = nrb;
+          if (l == 0) s_n[s] = shape_of(st, s).G;
+        }
+        int incl = items;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int y = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += y;
+        }
+        if (s < nb) s_pre[l * nb + s] = run + incl - items;
+        run += __shfl_sync(0xffffffffu, incl, 31);
+      }
+    }
+    for (int s = lane; s < nb; s += 32) s_ready[s] = 0;
+    if (lane == 0) {
+      s_pre[3 * nb] = run;
+      for (int i = 0; i < SC::kStages; ++i) {
+        mbar_init(&full[i], 1);
+        mbar_init(&empty[i], kWarps);
+      }
+      for (int i = 0; i < kDescRing; ++i) {
+        mbar_init(&dfull[i], 1);
+        mbar_init(&dempty[i], kWarps);
+      }
+      fence_barrier_init();
+    }
+  }
+  __syncthreads();
+  const int total = s_pre[3 * nb];
+  auto items_of = [&](int idx) { return s_pre[idx + 1] - s_pre[idx]; };
+
+  if (warp == kWarps) {
+    // ===================== producer: grab, resolve, issue =====================
+    int k = 0, di = 0;
+    auto post = [&](const FlowDesc& x) {
+      const int slot = di % kDescRing;
+      if (lane == 0) {
+        mbar_wait(&dempty[slot], (uint32_t)(((di / kDescRing) & 1) ^ 1));
+        desc[slot] = x;
+        mbar_arrive(&dfull[slot]);
+      }
+      __syncwarp();
+      ++di;
+    };
+    // Items are grabbed kGrab at a time: consecutive items of a (level, slot)
+    // share a slice (slice-major order), so the consumers' anchor slice stays
+    // in registers across a grab and the counter is hit once per kGrab items.
+    // Within a grab, groups of 4 items resolve their 32 row pointers in one
+    // round of loads (lane 8q + r: item q, row r) before any TMA is issued.
+    // The grab size follows the level the counter was last seen in (guided
+    // self-scheduling): a quarter of an even share, so a short level (the
+    // grids) still spreads over every CTA.
+    int grab_of[3];
+#pragma unroll
+    for (int l = 0; l < 3; ++l)
+      grab_of[l] = max(1, min(16, (s_pre[(l + 1) * nb] - s_pre[l * nb]) / (4 * (int)gridDim.x)));
+    int seen_level = 0;
+    bool finished = false;
+    while (!finished) {
+      const int kGrab = grab_of[seen_level];
+      int it0 = 0;
+      if (lane == 0) it0 = atomicAdd(next, kGrab);
+      it0 = __shfl_sync(0xffffffffu, it0, 0);
+      seen_level = it0 >= s_pre[2 * nb] ? 2 : (it0 >= s_pre[nb] ? 1 : 0);
+      for (int g0 = 0; g0 < kGrab && !finished; g0 += 4) {
+        int q_s[4], q_level[4], q_r0[4], q_rows[4], q_slice[4];
+        int nq = 0;
+        for (int q = 0; q < 4 && g0 + q < kGrab; ++q) {
+          const int it = it0 + g0 + q;
+          if (it >= total) {
+            finished = true;
+            break;
+          }
+          int lo = 0, hi = 3 * nb;  // last idx with s_pre[idx] <= it
+          while (hi - lo > 1) {
+            const int mid = (lo + hi) >> 1;
+            if (s_pre[mid] <= it) lo = mid; else hi = mid;
+          }
+          const int level = lo / nb, s = lo - level * nb;
+          if (level > 0 && s_ready[s] < level) {
+            int ready = 0;
+            if (lane == 0) ready = ld_acquire_gpu(&lvl[s]) >= level;
+            ready = __shfl_sync(0xffffffffu, ready, 0);
+            __syncwarp();  // order the lanes' candidate reads after lane 0's acquire
+            if (!ready) {
+              post(FlowDesc{0, 0, 0, kDescFlush, 0});  // consumers publish pending completions first
+              if (lane == 0) {
+                const uint64_t t0 = global_ns();
+                uint32_t polls = 0;
+                while (ld_acquire_gpu(&lvl[s]) < level) {
+                  if ((++polls & 1023u) == 0 && global_ns() - t0 > 4000000000ull) {
+                    printf("chess: select dataflow wait timed out (block %d slot %d level %d)\n", blockIdx.x, s, level);
+                    asm volatile("trap;");
+                  }
+                }
+              }
+              __syncwarp();
+            }
+            if (lane == 0) {
+              s_ready[s] = level;
+              s_n[level * nb + s] = __ldcg(&ws.cand_n[4 * s + level]);
+            }
+            __syncwarp();
+          }
+          const int n = s_n[level * nb + s];
+          const int nrb = s_nrb[lo];
+          const int local = it - s_pre[lo];
+          q_s[q] = s;
+          q_level[q] = level;
+          q_slice[q] = local / nrb;
+          q_r0[q] = (local - q_slice[q] * nrb) * kScanRows;
+          q_rows[q] = max(0, min(kScanRows, n - q_r0[q]));
+          ++nq;
+        }
+        // one round of row-pointer loads for the group
+        const int mq = lane >> 3, mr_ = lane & 7;
+        const T* src = nullptr;
+        uint32_t bytes = 0;
+        if (mq < nq) {
+          int qs = 0, ql = 0, qr0 = 0, qrows = 0, qsl = 0;
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            if (q == mq) {
+              qs = q_s[q]; ql = q_level[q]; qr0 = q_r0[q]; qrows = q_rows[q]; qsl = q_slice[q];
+            }
+          if (mr_ < qrows) {
+            const int64_t ebase = (int64_t)qsl * SC::kSlice;
+            bytes = (uint32_t)(min((int64_t)SC::kSlice, d.ld - ebase) * sizeof(T));
+            const LevelShape none = {0, 0, 0};  // only the full scan's level 3 needs the shape
+            src = level_row_ptr<T>(st, ws, qs, ql, qr0 + mr_, none) + ebase;
+          }
+        }
+        for (int q = 0; q < nq; ++q) {
+          post(FlowDesc{q_s[q], q_level[q], q_r0[q], q_rows[q], q_slice[q]});
+          if (mq == q && src) {
+            const int kr = k + mr_;
+            const int stage = kr % SC::kStages;
+            mbar_wait(&empty[stage], (uint32_t)(((kr / SC::kStages) & 1) ^ 1));
+            mbar_arrive_expect_tx(&full[stage], bytes);
+            tma_load_1d(ring + (size_t)stage * SC::kStageBytes, src, bytes, &full[stage]);
+          }
+          k += q_rows[q];
+          __syncwarp();
+        }
+      }
+    }
+    post(FlowDesc{0, 0, 0, kDescEnd, 0});
+    return;
+  }
+
+  // ===================== consumers =====================
+  if (blockIdx.x == 0) handle_empty_slots(st, ws, prm, sm);
+  int k = 0, di = 0, buf = 0;
+  int a_s = -1, a_slice = -1;
+  int run_idx = -1, run_cnt = 0;  // pending completions of (level, slot) index run_idx
+  double a[SC::kPerThread];
+  bool in[SC::kGroups];
+  bool all_in = true;
+  auto flush = [&]() {
+    if (run_idx < 0) return;
+    block_sync<kNT>();
+    if (threadIdx.x == 0) {
+      fence_acq_rel_gpu();
+      const int prev = atomicAdd(&done[run_idx], run_cnt);
+      s_last = (prev + run_cnt == items_of(run_idx));
+    }
+    block_sync<kNT>();
+    if (s_last) {
+      fence_acq_rel_gpu();
+      const int level = run_idx / nb, s = run_idx - level * nb;
+      const int n = level == 0 ? shape_of(st, s).G : __ldcg(&ws.cand_n[4 * s + level]);
+      if (n > 0) select_tail(st, ws, prm, s, level, n, sm);
+      if (threadIdx.x == 0 && level < 2) {
+        fence_acq_rel_gpu();
+        st_release_gpu(&lvl[s], level + 1);
+      }
+      block_sync<kNT>();
+    }
+    run_idx = -1;
+    run_cnt = 0;
+  };
+  for (;;) {
+    const int slot = di % kDescRing;
+    mbar_wait(&dfull[slot], (uint32_t)((di / kDescRing) & 1));
+    const FlowDesc x = desc[slot];
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&dempty[slot]);
+    ++di;
+    if (x.rows < 0) {
+      flush();
+      if (x.rows == kDescEnd) break;
+      continue;
+    }
+    const int idx = x.level * nb + x.s;
+    if (idx != run_idx) {
+      flush();
+      run_idx = idx;
+    }
+    ++run_cnt;
+    if (x.rows == 0) continue;
+    const int64_t ebase = (int64_t)x.slice * SC::kSlice;
+    if (x.s != a_s || x.slice != a_slice) {  // anchor slice (f64) in registers; zero beyond ld
+      a_s = x.s;
+      a_slice = x.slice;
+      const double* anc = st.anchor + (int64_t)x.s * d.ld + ebase;
+      all_in = ebase + SC::kSlice <= d.ld;
+#pragma unroll
+      for (int v = 0; v < SC::kGroups; ++v) {
+        const int o = SC::off(v);
+        in[v] = ebase + o < d.ld;
+#pragma unroll
+        for (int e = 0; e < SC::kVec; e += 2) {
+          double2 y = make_double2(0.0, 0.0);
+          if (in[v]) y = *reinterpret_cast<const double2*>(anc + o + e);
+          a[v * SC::kVec + e] = y.x;
+          a[v * SC::kVec + e + 1] = y.y;
+        }
+      }
+    }
+    double acc[kScanRows];
+#pragma unroll
+    for (int r = 0; r < kScanRows; ++r) {
+      acc[r] = 0.0;
+      if (r < x.rows) {
+        const int kr = k + r;
+        mbar_wait(&full[kr % SC::kStages], (uint32_t)((kr / SC::kStages) & 1));
+      }
+    }
+    {
+      uint32_t rowa[kScanRows];
+#pragma unroll
+      for (int r = 0; r < kScanRows; ++r)
+        rowa[r] = smem_u32(ring) + (uint32_t)(((k + r) % SC::kStages) * SC::kStageBytes);
+#pragma unroll
+      for (int v = 0; v < SC::kGroups; ++v) {
+        if (all_in || in[v]) {
+#pragma unroll
+          for (int r = 0; r < kScanRows; ++r) {
+            if (r < x.rows) {
+              const uint32_t ad = rowa[r] + (uint32_t)(SC::off(v) * sizeof(T));
+              if constexpr (sizeof(T) == 4) {
+                const float4 f = lds_f4(ad);
+                acc[r] = __fma_rn(a[4 * v + 0], (double)f.x, acc[r]);
+                acc[r] = __fma_rn(a[4 * v + 1], (double)f.y, acc[r]);
+                acc[r] = __fma_rn(a[4 * v + 2], (double)f.z, acc[r]);
+                acc[r] = __fma_rn(a[4 * v + 3], (double)f.w, acc[r]);
+              } else {
+                const double2 f = lds_d2(ad);
+                acc[r] = __fma_rn(a[2 * v + 0], f.x, acc[r]);
+                acc[r] = __fma_rn(a[2 * v + 1], f.y, acc[r]);
+              }
+            }
+          }
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) {
+#pragma unroll
+      for (int r = 0; r < kScanRows; ++r)
+        if (r < x.rows) mbar_arrive(&empty[(k + r) % SC::kStages]);
+    }
+    k += x.rows;
+    {  // warp transpose-reduce of 8 row partials (as in select_scan_kernel)
+      const bool b4 = lane & 16;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const double send = b4 ? acc[i] : acc[4 + i];
+        const double keep = b4 ? acc[4 + i] : acc[i];
+        acc[i] = keep + shfl_xor_d(send, 16);
+      }
+      const bool b3 = lane & 8;
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const double send = b3 ? acc[i] : acc[2 + i];
+        const double keep = b3 ? acc[2 + i] : acc[i];
+        acc[i] = keep + shfl_xor_d(send, 8);
+      }
+      const bool b2 = lane & 4;
+      {
+        const double send = b2 ? acc[0] : acc[1];
+        const double keep = b2 ? acc[1] : acc[0];
+        acc[0] = keep + shfl_xor_d(send, 4);
+      }
+      acc[0] += shfl_xor_d(acc[0], 2);
+      acc[0] += shfl_xor_d(acc[0], 1);
+      const int row = ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
+      if ((lane & 3) == 0) s_wpart[buf][row][warp] = acc[0];
+    }
+    block_sync<kNT>();
+    if ((int)threadIdx.x < x.rows) {
+      double y = s_wpart[buf][threadIdx.x][0];
+#pragma unroll
+      for (int w = 1; w < kWarps; ++w) y = __dadd_rn(y, s_wpart[buf][threadIdx.x][w]);
+      ws.part[((int64_t)x.s * mr + x.r0 + threadIdx.x) * nsl + x.slice] = y;
+    }
+    buf ^= 1;
+  }
+}
+
+// ---------------------------------------------------------------------------
 // KV-head shard: finish one level from every rank's exported
 // partial scores.  gathered = [world][batch][xld] (rank-major, the layout of
 // an all-gather of each rank's xout); the partials are added in rank order so
@@ -883,9 +1264,40 @@ static int launch_scan(const ChessState& st, const Workspace& ws, const SelParam
   return check_launch("select_scan");
 }
 
+template <typename T>
+static size_t flow_smem(int batch) {
+  using SC = ScanCfg<T>;
+  return 128 + (size_t)SC::kStages * SC::kStageBytes + 2 * SC::kStages * 8 + 2 * kDescRing * 8 +
+         kDescRing * sizeof(FlowDesc) + (size_t)(10 * batch + 1) * sizeof(int);
+}
+
+template <typename T>
+static int launch_flow(const ChessState& st, const Workspace& ws, const SelParams& prm,
+                       cudaStream_t stream) {
+  const size_t smem = flow_smem<T>(st.d.batch);
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(select_flow_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)flow_smem<T>(kFlowMaxBatch));
+    configured = true;
+  }
+  // scheduler counters start at zero every call (a memset node under capture)
+  cudaMemsetAsync(ws.flow, 0, (size_t)(1 + 4 * st.d.batch) * sizeof(int32_t), stream);
+  select_flow_kernel<T><<<num_sms(), kScanCTA, smem, stream>>>(st, ws, prm);
+  return check_launch("select_flow");
+}
+
 // persistent scan: one CTA per SM (192 KB TMA ring each), one launch per level
 int launch_select(const ChessState& st, const Workspace& ws, const SelParams& prm, int /*grid*/,
                   cudaStream_t stream) {
+  // Dataflow cascade (one launch), opt-in: CHESS_SELECT_FLOW=1.  Parity-green
+  // (tests/test_gpu_select.py, test_gpu_pagesel.py, test_gpu_headshard.py) but
+  // measured slower than three per-level launches (tools/select_micro.py:
+  // cfg3 378 vs 308 us, cfg2 45 vs 38 us) — kept for further work.
+  static const int flow_env = getenv("CHESS_SELECT_FLOW") ? atoi(getenv("CHESS_SELECT_FLOW")) : 0;
+  if (flow_env && !prm.full_scan && !prm.xout && prm.mode == 0 && st.d.batch <= kFlowMaxBatch)
+    return st.d.summary_dtype == 0 ? launch_flow<float>(st, ws, prm, stream)
+                                   : launch_flow<double>(st, ws, prm, stream);
   const int nlev = prm.full_scan ? 1 : 3;
   for (int li = 0; li < nlev; ++li) {
     const int level = prm.full_scan ? 3 : li;
