@@ -2,8 +2,9 @@
 us/step (select+attn) at 1% KV; % HBM roofline).
 
 A step = one decode token for every sequence of the batch through the
-device engine: KV append -> L x sparse paged decode -> entropy + trigger ->
-summary seal -> selection cascade.  Headline variant: selection forced on
+device engine: KV append -> entropy + trigger -> summary seal -> {selection
+cascade on a side stream || L x sparse paged decode} -> working-set flush
+(engine.ChessDecoder.step; sequential order for a head-shard exchange).  Headline variant: selection forced on
 every step (worst case); the dynamic (backtracking) and
 attention-only variants are reported alongside.
 

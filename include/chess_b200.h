@@ -32,7 +32,7 @@
 extern "C" {
 #endif
 
-#define CHESS_ABI_VERSION 2
+#define CHESS_ABI_VERSION 3
 
 /* Status codes.  Python shim maps them to the pagesel exception classes
  * (pagesel/errors.py:4-21 and the ValueError/IndexError sites listed). */
@@ -156,6 +156,11 @@ typedef struct ChessSelectCfg {
   double rho_page;
   int32_t full_scan;
   int32_t force_all;     /* ignore fire[] and select for every slot */
+  int32_t defer_ws;      /* 1: write the semantic sets but leave working sets and
+                          * block tables untouched (marked pending) until
+                          * chess_flush_working_sets, so the pass can run
+                          * concurrently with sparse_decode reading them */
+  int32_t pad_;
 } ChessSelectCfg;
 
 /* Trigger knobs (uncertainty.py:86-98, simulate.py:163-170). */
@@ -261,6 +266,9 @@ int chess_select_combine(const ChessState* st, const ChessSelectCfg* cfg, int32_
 /* K3 epilogue alone: rebuild working set + block table from the cached
  * semantic set for all slots (selection.py:126-140). */
 int chess_build_working_set(const ChessState* st, void* stream);
+
+/* ... for the slots a defer_ws selection pass marked pending only. */
+int chess_flush_working_sets(const ChessState* st, void* stream);
 
 /* K4: sparse paged decode attention for one layer over the block table.
  * q: bf16 [batch][q_heads][head_dim] with batch stride q_stride (elements);

@@ -21,7 +21,7 @@ from .errors import (
 )
 
 LIB_PATH = Path(__file__).resolve().parent / "libchess_b200.so"
-ABI_VERSION = 2
+ABI_VERSION = 3
 
 # enum ChessStatus
 OK, ERR_CONFIG, ERR_OUT_OF_PAGES, ERR_EMPTY_CONTEXT, ERR_SHAPE, ERR_INDEX, ERR_ORDER, ERR_VALUE, ERR_CUDA, ERR_UNSUPPORTED = range(10)
@@ -78,6 +78,8 @@ class ChessSelectCfg(C.Structure):
         ("rho_page", C.c_double),
         ("full_scan", C.c_int32),
         ("force_all", C.c_int32),
+        ("defer_ws", C.c_int32),
+        ("pad_", C.c_int32),
     ]
 
 
@@ -119,6 +121,7 @@ SIGNATURES = {
     "chess_select_partial": (C.c_int, [C.POINTER(ChessState), C.POINTER(ChessSelectCfg), _I32, _P, _I64, _P]),
     "chess_select_combine": (C.c_int, [C.POINTER(ChessState), C.POINTER(ChessSelectCfg), _I32, _P, _I32, _I64, _P]),
     "chess_build_working_set": (C.c_int, [C.POINTER(ChessState), _P]),
+    "chess_flush_working_sets": (C.c_int, [C.POINTER(ChessState), _P]),
     "chess_sparse_decode": (C.c_int, [C.POINTER(ChessState), _I32, _P, _I64, _P, _I64, _P, _F, _P]),
     "chess_entropy_trigger": (C.c_int, [C.POINTER(ChessState), _P, _I64, _I64, C.POINTER(ChessTriggerCfg), _P, _P]),
     "chess_record_entropy": (C.c_int, [C.POINTER(ChessState), _P, _P, C.POINTER(ChessTriggerCfg), _P]),

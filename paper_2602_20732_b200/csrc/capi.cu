@@ -20,6 +20,7 @@ int launch_from_vectors(const ChessState&, int, const double*, int, int64_t, con
                         cudaStream_t);
 int launch_mean_rows(const void*, int, int64_t, int64_t, int64_t, double*, cudaStream_t);
 int launch_select(const ChessState&, const Workspace&, const SelParams&, int, cudaStream_t);
+int launch_flush_ws(const ChessState&, const Workspace&, cudaStream_t);
 int launch_pool_init(const ChessState&, const int32_t*, int, cudaStream_t);
 int launch_pool_reserve(const ChessState&, const int32_t*, cudaStream_t);
 int launch_pool_release(const ChessState&, const uint8_t*, cudaStream_t);
@@ -105,6 +106,7 @@ size_t workspace_layout(const ChessDims& d, void* base, Workspace* ws) {
     return o;
   };
   const size_t o_sel_done = take(b * 4);
+  const size_t o_ws_pending = take(b * 4);
   const size_t o_flow = take((1 + 4 * b) * 4);
   const size_t o_cand = take(b * 3 * mr * 4);
   const size_t o_cand_n = take(b * 4 * 4);
@@ -122,6 +124,7 @@ size_t workspace_layout(const ChessDims& d, void* base, Workspace* ws) {
   if (ws && base) {
     uint8_t* p = reinterpret_cast<uint8_t*>(base);
     ws->sel_done = reinterpret_cast<int32_t*>(p + o_sel_done);
+    ws->ws_pending = reinterpret_cast<int32_t*>(p + o_ws_pending);
     ws->flow = reinterpret_cast<int32_t*>(p + o_flow);
     ws->cand = reinterpret_cast<int32_t*>(p + o_cand);
     ws->cand_n = reinterpret_cast<int32_t*>(p + o_cand_n);
@@ -281,6 +284,7 @@ static int select_params(const ChessSelectCfg* cfg, SelParams* out) {
   static const int dbg_mode = getenv("CHESS_SELECT_MODE") ? atoi(getenv("CHESS_SELECT_MODE")) : 0;
   prm.mode = dbg_mode;
   prm.force_all = cfg->force_all;
+  prm.defer_ws = cfg->defer_ws;
   *out = prm;
   return CHESS_OK;
 }
@@ -363,6 +367,13 @@ int chess_pool_release(const ChessState* st, const uint8_t* mask, void* stream) 
   int rc = pool_state(st);
   if (rc) return rc;
   return launch_pool_release(*st, mask, (cudaStream_t)stream);
+}
+
+int chess_flush_working_sets(const ChessState* st, void* stream) {
+  Workspace ws;
+  int rc = state_ws(st, &ws);
+  if (rc) return rc;
+  return launch_flush_ws(*st, ws, (cudaStream_t)stream);
 }
 
 int chess_build_working_set(const ChessState* st, void* stream) {

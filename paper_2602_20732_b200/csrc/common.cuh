@@ -58,6 +58,7 @@ constexpr bool kTrace = CHESS_TRACE != 0;
 
 struct Workspace {
   int32_t* sel_done;     // [batch]
+  int32_t* ws_pending;   // [batch] working set owed by a defer_ws selection pass
   int32_t* flow;         // select dataflow scheduler: [0] next item, [1 .. 3b] items done per
                          // (level, slot), [1+3b .. 1+4b] levels finished per slot
   int32_t* cand;         // [batch][3][max_rows]  candidate row ids per level
@@ -88,6 +89,7 @@ struct SelParams {
   int32_t full_scan;
   int32_t force_all;
   int32_t mode;  // debug (CHESS_SELECT_MODE): 0 normal, 1 no math, 2 no loads
+  int32_t defer_ws;  // leave working sets to chess_flush_working_sets (concurrent step)
   // KV-head shard: when set, the level's tail stops after the
   // fixed-order slice reduction and exports this rank's PARTIAL scores to
   // xout[slot * xld + candidate]; select_combine_kernel finishes the level.

@@ -1038,7 +1038,8 @@ int launch_sparse_decode(const ChessState& st, const Workspace& ws, int layer, c
   static const int prefetch = getenv("CHESS_ATTN_PREFETCH") ? atoi(getenv("CHESS_ATTN_PREFETCH")) : 0;
   a.prefetch = prefetch;
   const int gq = d.q_heads / d.kv_heads;
-  const int nctas = ws.attn_ctas;
+  static const int grid_env = getenv("CHESS_ATTN_GRID") ? atoi(getenv("CHESS_ATTN_GRID")) : 0;  // experiments
+  const int nctas = grid_env > 0 ? std::min(grid_env, ws.attn_ctas) : ws.attn_ctas;
   if ((reinterpret_cast<uintptr_t>(q) & 15) || (q_stride & 7))
     return fail(CHESS_ERR_UNSUPPORTED, "sparse_decode: q must be 16-byte aligned with q_stride %% 8 == 0");
   if (d.kv_heads > 255 || d.batch > kAttnMaxBatch)

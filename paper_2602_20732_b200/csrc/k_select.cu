@@ -249,7 +249,13 @@ __device__ void select_tail_topk(const ChessState& st, const Workspace& ws, cons
     block_sync<kNT>();
     __threadfence_block();
   }
-  if (lv_end == 3) block_build_ws<kNT>(st, s, sm.scratch);
+  if (lv_end == 3) {
+    if (prm.defer_ws) {  // the block table is being read by a concurrent decode
+      if (threadIdx.x == 0) ws.ws_pending[s] = 1;
+    } else {
+      block_build_ws<kNT>(st, s, sm.scratch);
+    }
+  }
 }
 
 // slots that fired with an empty index: empty semantic set + WS refresh
@@ -264,7 +270,11 @@ __device__ void handle_empty_slots(const ChessState& st, const Workspace& ws, co
       for (int i = 0; i < 8; ++i) st.sel_stats[8 * s + i] = 0;
     }
     block_sync<kNT>();
-    block_build_ws<kNT>(st, s, sm.scratch);
+    if (prm.defer_ws) {
+      if (threadIdx.x == 0) ws.ws_pending[s] = 1;
+    } else {
+      block_build_ws<kNT>(st, s, sm.scratch);
+    }
   }
 }
 
@@ -1375,6 +1385,21 @@ __global__ void __launch_bounds__(256) build_ws_kernel(ChessState st) {
   block_build_ws<256>(st, blockIdx.x, s_scr);
 }
 }  // namespace
+
+namespace {
+__global__ void __launch_bounds__(256) flush_ws_kernel(ChessState st, Workspace ws) {
+  __shared__ int s_scr[64];
+  const int s = blockIdx.x;
+  if (!ws.ws_pending[s]) return;
+  block_build_ws<256>(st, s, s_scr);
+  if (threadIdx.x == 0) ws.ws_pending[s] = 0;
+}
+}  // namespace
+
+int launch_flush_ws(const ChessState& st, const Workspace& ws, cudaStream_t stream) {
+  flush_ws_kernel<<<st.d.batch, 256, 0, stream>>>(st, ws);
+  return check_launch("flush_working_sets");
+}
 
 int launch_build_ws_all(const ChessState& st, cudaStream_t stream) {
   build_ws_kernel<<<st.d.batch, 256, 0, stream>>>(st);

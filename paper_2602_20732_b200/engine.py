@@ -70,6 +70,7 @@ class ChessDecoder:
         full_scan=False,
         softmax_scale=None,
         exchange=None,
+        concurrent_select=None,
     ):
         from .errors import ConfigurationError
 
@@ -94,6 +95,13 @@ class ChessDecoder:
         self.sel_cfg_all = _lib.ChessSelectCfg(
             config.rho_grid, config.rho_chunk, config.rho_page, 1 if full_scan else 0, 1
         )
+        # defer_ws twins: the pass leaves working sets pending (concurrent step)
+        self.sel_cfg_defer = _lib.ChessSelectCfg(
+            config.rho_grid, config.rho_chunk, config.rho_page, 1 if full_scan else 0, 0, 1
+        )
+        self.sel_cfg_all_defer = _lib.ChessSelectCfg(
+            config.rho_grid, config.rho_chunk, config.rho_page, 1 if full_scan else 0, 1, 1
+        )
         self.trig_cfg = _lib.ChessTriggerCfg()
         self.trig_cfg.policy = _POLICY_CODE[kind]
         self.trig_cfg.interval = interval or 1
@@ -108,6 +116,18 @@ class ChessDecoder:
         self.exchange = exchange
         if exchange is not None and exchange.levels != ([3] if full_scan else [0, 1, 2]):
             raise ConfigurationError("exchange and decoder disagree on full_scan")
+        # Selection of step t only feeds step t+1's decode, so it can run on a
+        # side stream concurrently with step t's L decode launches (it fills
+        # the SMs and HBM left idle at layer boundaries); its working-set /
+        # block-table writes are deferred to chess_flush_working_sets after the
+        # join.  Not with a head-shard exchange: two streams of NCCL calls per
+        # rank could interleave differently across ranks.
+        if concurrent_select is None:
+            concurrent_select = exchange is None
+        if concurrent_select and exchange is not None:
+            raise ConfigurationError("concurrent selection cannot be combined with a head-shard exchange")
+        self.concurrent_select = bool(concurrent_select)
+        self._side = torch.cuda.Stream(device=state.device) if self.concurrent_select else None
 
     # ------------------------------------------------------------------
     # prefill: KV rows already in the pool, page tables/counters set
@@ -116,8 +136,11 @@ class ChessDecoder:
         """K1b: index pages [0, n_pages[s]) of every slot (prefill)."""
         _lib.call("chess_summary_build", self.state.ref, _lib.ptr(n_pages), _lib.stream_ptr(stream))
 
-    def select(self, force_all=False, stream=None):
-        cfg = self.sel_cfg_all if force_all else self.sel_cfg
+    def select(self, force_all=False, stream=None, defer_ws=False):
+        if defer_ws:
+            cfg = self.sel_cfg_all_defer if force_all else self.sel_cfg_defer
+        else:
+            cfg = self.sel_cfg_all if force_all else self.sel_cfg
         x = self.exchange
         if x is None:
             _lib.call("chess_select", self.state.ref, C.byref(cfg), _lib.stream_ptr(stream))
@@ -182,6 +205,9 @@ class ChessDecoder:
         block and the exchange all-gathers it after every layer."""
         x = self.exchange
         self.append(k_new, v_new, stream)
+        if self.concurrent_select and self.kind != "never":
+            self._step_concurrent(q, logits, out, lse, entropy_out, stream)
+            return
         for layer in range(self.state.shape.layers):
             o = out[:, layer] if x is None else out[layer, x.rank]
             self.attend(layer, q[:, layer], o, None if lse is None else lse[layer], stream)
@@ -192,6 +218,26 @@ class ChessDecoder:
         self.seal(stream)
         if self.kind != "never":
             self.select(force_all=False, stream=stream)
+
+    def _step_concurrent(self, q, logits, out, lse, entropy_out, stream):
+        """entropy -> seal, then [selection (side stream, deferred working
+        sets) || L x decode], join, flush the pending working sets.  Same
+        results as the sequential order: the decode reads only KV, q and the
+        block table, none of which entropy/seal/selection write before the
+        flush."""
+        cur = stream if stream is not None else torch.cuda.current_stream()
+        self.entropy_trigger(logits, entropy_out, cur)
+        self.seal(cur)
+        fork = torch.cuda.Event()
+        fork.record(cur)
+        self._side.wait_event(fork)
+        self.select(force_all=False, stream=self._side, defer_ws=True)
+        for layer in range(self.state.shape.layers):
+            self.attend(layer, q[:, layer], out[:, layer], None if lse is None else lse[layer], cur)
+        join = torch.cuda.Event()
+        join.record(self._side)
+        cur.wait_event(join)
+        _lib.call("chess_flush_working_sets", self.state.ref, _lib.stream_ptr(cur))
 
     # ------------------------------------------------------------------
     def capture(self, k_new, v_new, q, logits, out, lse=None, entropy_out=None):
