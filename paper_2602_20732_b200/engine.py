@@ -220,22 +220,23 @@ class ChessDecoder:
             self.select(force_all=False, stream=stream)
 
     def _step_concurrent(self, q, logits, out, lse, entropy_out, stream):
-        """entropy -> seal, then [selection (side stream, deferred working
-        sets) || L x decode], join, flush the pending working sets.  Same
-        results as the sequential order: the decode reads only KV, q and the
-        block table, none of which entropy/seal/selection write before the
+        """fork { side: entropy+trigger -> seal -> selection (working sets
+        deferred) || main: L x decode }, join, flush the pending working sets.
+        Same results as the sequential order: the decode reads only KV, q and
+        the block table, none of which the side stream writes before the
         flush."""
         cur = stream if stream is not None else torch.cuda.current_stream()
-        self.entropy_trigger(logits, entropy_out, cur)
-        self.seal(cur)
         fork = torch.cuda.Event()
         fork.record(cur)
-        self._side.wait_event(fork)
-        self.select(force_all=False, stream=self._side, defer_ws=True)
+        side = self._side
+        side.wait_event(fork)
+        self.entropy_trigger(logits, entropy_out, side)
+        self.seal(side)
+        self.select(force_all=False, stream=side, defer_ws=True)
         for layer in range(self.state.shape.layers):
             self.attend(layer, q[:, layer], out[:, layer], None if lse is None else lse[layer], cur)
         join = torch.cuda.Event()
-        join.record(self._side)
+        join.record(side)
         cur.wait_event(join)
         _lib.call("chess_flush_working_sets", self.state.ref, _lib.stream_ptr(cur))
 
