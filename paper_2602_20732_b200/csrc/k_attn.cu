@@ -54,7 +54,12 @@ constexpr int kThreads = (kConsumers + 1) * 32;
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kLn2 = 0.6931471805599453f;
 // per-CTA dynamic smem budget at CPS CTAs per SM, minus reserved + static smem
-__host__ __device__ constexpr int smem_budget(int cps) { return (228 * 1024) / cps - 1024 - 256; }
+#ifndef CHESS_ATTN_SMEM_KB  // experiment knob: cap the per-CTA budget (co-residency studies)
+#define CHESS_ATTN_SMEM_KB 228
+#endif
+__host__ __device__ constexpr int smem_budget(int cps) {
+  return (cps == 1 && CHESS_ATTN_SMEM_KB < 228 ? CHESS_ATTN_SMEM_KB : 228) * 1024 / cps - 1024 - 256;
+}
 
 struct AttnArgs {
   const __nv_bfloat16* q;

@@ -290,6 +290,14 @@ __device__ void handle_empty_slots(const ChessState& st, const Workspace& ws, co
 // through the per-slot tails, so HBM never idles on the epilogues.
 // ---------------------------------------------------------------------------
 constexpr int kScanCTA = kNT + 32;  // 8 consumer warps + 1 producer warp
+// Experiment knobs (co-residency with the decode kernel): TMA ring size and
+// the min-blocks launch bound (2 caps registers at 113/thread).
+#ifndef CHESS_SCAN_RING_KB
+#define CHESS_SCAN_RING_KB 192
+#endif
+#ifndef CHESS_SCAN_MINB
+#define CHESS_SCAN_MINB 1
+#endif
 
 // Debug timeline (chess_debug_select_trace): per CTA of the last launch of
 // each level, {entry, prologue, first row, items done, exit, wait cycles of
@@ -303,7 +311,7 @@ template <typename T>
 struct ScanCfg {
   static constexpr int kSlice = kScanSliceBytes / (int)sizeof(T);   // elements per row slice
   static constexpr int kStageBytes = kScanSliceBytes;
-  static constexpr int kStages = (192 * 1024) / kStageBytes;
+  static constexpr int kStages = (CHESS_SCAN_RING_KB * 1024) / kStageBytes;
   static constexpr int kVec = 16 / (int)sizeof(T);                // elements per 16-B chunk
   static constexpr int kPerThread = kSlice / kNT;                  // elements per thread
   static constexpr int kGroups = kPerThread / kVec;                // chunks per thread
@@ -311,7 +319,7 @@ struct ScanCfg {
 };
 
 template <typename T>
-__global__ void __launch_bounds__(kScanCTA, 1) select_scan_kernel(ChessState st, Workspace ws,
+__global__ void __launch_bounds__(kScanCTA, CHESS_SCAN_MINB) select_scan_kernel(ChessState st, Workspace ws,
                                                                   SelParams prm, int level) {
   using SC = ScanCfg<T>;
   extern __shared__ uint8_t smem_raw[];
@@ -319,7 +327,7 @@ __global__ void __launch_bounds__(kScanCTA, 1) select_scan_kernel(ChessState st,
   uint64_t* full = reinterpret_cast<uint64_t*>(ring + (size_t)SC::kStages * SC::kStageBytes);
   uint64_t* empty = full + SC::kStages;
   int* s_prefix = reinterpret_cast<int*>(empty + SC::kStages);  // [batch + 1]
-  int* s_rows = s_prefix + kMaxBatch + 1;                        // [batch] candidate rows
+  int* s_rows = s_prefix + st.d.batch + 1;                       // [batch] candidate rows
   __shared__ double s_wpart[2][kScanRows][kWarps];
   __shared__ TailSmem sm;
   __shared__ int s_last;
@@ -1261,7 +1269,7 @@ static int launch_scan(const ChessState& st, const Workspace& ws, const SelParam
                        cudaStream_t stream) {
   using SC = ScanCfg<T>;
   const size_t smem = 128 + (size_t)SC::kStages * SC::kStageBytes + 2 * SC::kStages * 8 +
-                      (size_t)(2 * kMaxBatch + 1) * sizeof(int);
+                      (size_t)(2 * st.d.batch + 1) * sizeof(int);
   static bool configured = false;
   if (!configured) {
     const size_t smem_max = 128 + (size_t)SC::kStages * SC::kStageBytes + 2 * SC::kStages * 8 +
