@@ -46,6 +46,14 @@ namespace {
 #ifndef CHESS_ATTN_CONSUMERS
 #define CHESS_ATTN_CONSUMERS 4
 #endif
+// Pages per producer TMA run (<= 8: 4 lanes per page).  A run is issued only
+// once all its stages are free, so long runs make the producer wait for the
+// slowest consumer; measured (profiles/r01/attn_micro/sweep_producer_run.txt):
+// 8 -> 3 pages: cfg3 19.0 -> 18.25 us, cfg5 14.5 -> 13.0 us, cfg4 unchanged;
+// 1 page is slower (21.3 us).
+#ifndef CHESS_ATTN_RUN
+#define CHESS_ATTN_RUN 3
+#endif
 constexpr int kConsumers = CHESS_ATTN_CONSUMERS;
 constexpr int kMaxCtasPerSm = 2;
 constexpr int kAttnMaxBatch = 256;  // per-slot tables live in smem
@@ -427,7 +435,7 @@ __global__ void __launch_bounds__(kThreads, CPS)
       // page order, so the 2-slot q ring cannot deadlock).  Within a run,
       // lane 4p+b issues box b of page p: the TMA issues run in parallel.
       const uint32_t starts = __ballot_sync(0xffffffffu, cur_tag >= 0);
-      constexpr int kRun = C::kStages < 8 ? C::kStages : 8;  // distinct stages within a run
+      constexpr int kRun = C::kStages < CHESS_ATTN_RUN ? C::kStages : CHESS_ATTN_RUN;  // distinct stages within a run
       for (int c0 = 0; c0 < cnt;) {
         const uint32_t later = starts & ~((2u << c0) - 1u);  // starts after c0
         const int nxt_start = later ? __ffs(later) - 1 : 32;
