@@ -436,7 +436,9 @@ def run_gpu(args):
             "h2d_bytes_per_step": h2d,
             "d2h_bytes_per_step": d2h,
         },
-        "gpu_launches": args.steps * (L + 6 + (3 if head else 0)),  # + select_combine per level
+        # per step: append, entropy, seal, 3 select levels, L decode launches,
+        # + working-set flush (concurrent step) or + 3 select_combine (head shard)
+        "gpu_launches": args.steps * (L + 6 + (3 if head else 1)),
         "clocks": head["clocks"],
     }
     if not args.headline_only:
