@@ -141,7 +141,9 @@ def run_gpu(args):
     peak_src = "measured" if "hbm_gbs" in peaks else "fallback"
 
     cfg_name = args.config
-    c = CONFIGS[cfg_name]
+    c = dict(CONFIGS[cfg_name])
+    if args.page_size:
+        c["page"] = args.page_size
     batch = c["batch"] if args.batch is None else args.batch
     # sharding: cfg4 splits its batch across ranks, cfg5 its KV
     # heads; other configs run one replica per rank (weak scaling)
@@ -156,7 +158,7 @@ def run_gpu(args):
     gen_pages = math.ceil((total_steps + 2 * ring + 64) / c["page"]) + 4
     wl = SyntheticDecode(cfg_name, batch=batch, gen_pages=gen_pages, ring=ring, seed=rank,
                          summary_dtype=args.summary_dtype, head_shard=(rank, world) if head else None,
-                         kv_budget_gib=args.kv_gib)
+                         kv_budget_gib=args.kv_gib, page_size=args.page_size)
     st = wl.st
     sh = wl.shape
     sel = preset_config("aggressive", page_size=sh.page_size)
@@ -566,6 +568,7 @@ def main():
     ap.add_argument("--full-scan", action="store_true")
     ap.add_argument("--headline-only", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--page-size", type=int, default=None, help="override the config's page size (16/32)")
     ap.add_argument("--kv-gib", type=float, default=None,
                     help="KV pool budget per GPU (default: all free HBM minus headroom)")
     ap.add_argument("--shard", default="auto", choices=["auto", "batch", "head", "replica"],

@@ -83,8 +83,10 @@ class SyntheticDecode:
 
     def __init__(self, cfg_name="cfg3", batch=None, gen_pages=128, ring=64, seed=0,
                  device="cuda", summary_dtype="f32", kv_budget_gib=None, unstable_every=2,
-                 window=4, nc=8, ng=8, head_shard=None):
+                 window=4, nc=8, ng=8, head_shard=None, page_size=None):
         c = dict(CONFIGS[cfg_name])
+        if page_size is not None:  # page-size sweep (32 default, 16 swept)
+            c["page"] = page_size
         if head_shard is not None:
             # KV-head shard: this rank's kv / q heads of every layer
             _, world = head_shard
