@@ -690,7 +690,12 @@ __global__ void __launch_bounds__(kThreads, CPS)
     const long long ck2 = kTrace ? clock64() : 0;
     if (last) {
       // ---- this warp merges the piece (warp order, deterministic) ----
+      // writers: lanes' stores -> __syncwarp -> lane 0 fence.cta + atomic;
+      // reader: lane 0 atomic -> fence.cta -> __syncwarp -> lanes' loads.
+      // (compute-sanitizer racecheck models barriers, not fence+atomic
+      // handoffs, and reports this exchange as a hazard.)
       __threadfence_block();
+      __syncwarp();
       const int hh = (lane * C::kEPL) / HD, el = (lane * C::kEPL) % HD;
       float M = -INFINITY, L = 0.f, acc[C::kEPL];
 #pragma unroll
