@@ -348,6 +348,16 @@ int chess_entropy_logits(const float* logits, int64_t rows, int64_t vocab, int64
  * NumPy pairwise summation order. */
 int chess_page_uncertainty(const double* ent, int32_t n, double* out, void* stream);
 
+/* calibrate (uncertainty.py:59-83) on the device: page_uncertainty of every
+ * page's per-token entropies (entropies [n_pages][ld] f64, counts[p] >= 1
+ * entries in row p, device), then the nearest-rank percentile
+ * (rank = ceil(percentile * n_pages), uncertainty.py:59-61) of the page means
+ * and, independently, of the variances.  out = {tau_H, tau_V} (device f64).
+ * workspace >= chess_calibrate_workspace_bytes(n_pages). */
+size_t chess_calibrate_workspace_bytes(int32_t n_pages);
+int chess_calibrate(const double* entropies, const int32_t* counts, int32_t n_pages, int64_t ld,
+                    double percentile, double* out, void* workspace, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

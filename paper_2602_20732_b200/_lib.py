@@ -135,6 +135,8 @@ SIGNATURES = {
     "chess_entropy_workspace_bytes": (C.c_size_t, [_I64]),
     "chess_entropy_logits": (C.c_int, [_P, _I64, _I64, _I64, _P, _P, _P]),
     "chess_page_uncertainty": (C.c_int, [_P, _I32, _P, _P]),
+    "chess_calibrate_workspace_bytes": (C.c_size_t, [_I32]),
+    "chess_calibrate": (C.c_int, [_P, _P, _I32, _I64, _D, _P, _P, _P]),
 }
 
 _lib = None

@@ -21,6 +21,8 @@ int launch_from_vectors(const ChessState&, int, const double*, int, int64_t, con
 int launch_mean_rows(const void*, int, int64_t, int64_t, int64_t, double*, cudaStream_t);
 int launch_select(const ChessState&, const Workspace&, const SelParams&, int, cudaStream_t);
 int launch_flush_ws(const ChessState&, const Workspace&, cudaStream_t);
+size_t calibrate_workspace_bytes(int n);
+int launch_calibrate(const double*, const int32_t*, int, int64_t, int, double*, void*, cudaStream_t);
 int launch_pool_init(const ChessState&, const int32_t*, int, cudaStream_t);
 int launch_pool_reserve(const ChessState&, const int32_t*, cudaStream_t);
 int launch_pool_release(const ChessState&, const uint8_t*, cudaStream_t);
@@ -475,6 +477,24 @@ int chess_entropy_logits(const float* logits, int64_t rows, int64_t vocab, int64
   ws.ent_done = reinterpret_cast<int32_t*>(p);
   ws.ent_part = reinterpret_cast<double*>(p + ((rows * 4 + 255) / 256) * 256);
   return launch_entropy_logits(ws, logits, rows, vocab, ld, out, (cudaStream_t)stream);
+}
+
+size_t chess_calibrate_workspace_bytes(int32_t n_pages) {
+  return n_pages > 0 ? calibrate_workspace_bytes(n_pages) : 0;
+}
+
+int chess_calibrate(const double* entropies, const int32_t* counts, int32_t n_pages, int64_t ld,
+                    double percentile, double* out, void* workspace, void* stream) {
+  // CalibrationError cases (uncertainty.py:66-69) -> ValueError status
+  if (n_pages < 1) return fail(CHESS_ERR_VALUE, "cannot calibrate on an empty sample");
+  if (!(percentile > 0.0 && percentile < 1.0))
+    return fail(CHESS_ERR_VALUE, "percentile must be in (0, 1), got %g", percentile);
+  if (!entropies || !counts || !out || !workspace) return fail(CHESS_ERR_SHAPE, "calibrate: null buffer");
+  if (ld < 1) return fail(CHESS_ERR_SHAPE, "calibrate: bad row stride");
+  // nearest rank, ceil in double as math.ceil(percentile * len) (uncertainty.py:60)
+  int rank = (int)ceil(percentile * (double)n_pages);
+  rank = rank < 1 ? 1 : rank;
+  return launch_calibrate(entropies, counts, n_pages, ld, rank, out, workspace, (cudaStream_t)stream);
 }
 
 int chess_page_uncertainty(const double* ent, int32_t n, double* out, void* stream) {

@@ -276,7 +276,69 @@ __global__ void page_uncertainty_kernel(const double* e, int n, double* out) {
   out[1] = var;
 }
 
+// calibrate: page statistics, one thread per page (NumPy pairwise order)
+__global__ void calib_stats_kernel(const double* e, const int32_t* counts, int n_pages, int64_t ld,
+                                   double* means, double* vars) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n_pages) return;
+  const double* row = e + (int64_t)p * ld;
+  const int n = counts[p];
+  const double mean = __ddiv_rn(np_pairwise_sum(row, n, 1), (double)n);
+  const double var = __ddiv_rn(np_pairwise(
+                                   [=](int i) {
+                                     const double dlt = __dsub_rn(row[i], mean);
+                                     return __dmul_rn(dlt, dlt);
+                                   },
+                                   n),
+                               (double)n);
+  means[p] = mean;
+  vars[p] = var;
+}
+
+// nearest rank r (1-based) of x[0..n): the r-th smallest is the minimum of
+// the n - r + 1 largest (block radix top-k, K3's block_topk_mark).
+// blockIdx.x 0: means -> out[0], 1: variances -> out[1].
+__global__ void __launch_bounds__(kNT) calib_rank_kernel(const double* vals, int n, int r,
+                                                         uint64_t* keys, int* kept, double* out) {
+  __shared__ int s_hist[256];
+  __shared__ int s_scr[64];
+  __shared__ double s_min[kNT / 32];
+  const double* x = vals + (int64_t)blockIdx.x * n;
+  uint64_t* k = keys + (int64_t)blockIdx.x * n;
+  int* kp = kept + (int64_t)blockIdx.x * n;
+  for (int i = threadIdx.x; i < n; i += kNT) k[i] = score_key(x[i]);
+  __syncthreads();
+  block_topk_mark<kNT>(k, n, n - r + 1, kp, s_hist, s_scr);
+  double m = INFINITY;
+  for (int i = threadIdx.x; i < n; i += kNT)
+    if (kp[i]) m = fmin(m, x[i]);
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) m = fmin(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) s_min[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double v = s_min[0];
+    for (int w = 1; w < kNT / 32; ++w) v = fmin(v, s_min[w]);
+    out[blockIdx.x] = v;
+  }
+}
+
 }  // namespace
+
+size_t calibrate_workspace_bytes(int n) { return (size_t)n * (2 * 8 + 2 * 8 + 2 * 4) + 256; }
+
+int launch_calibrate(const double* e, const int32_t* counts, int n, int64_t ld, int rank, double* out,
+                     void* workspace, cudaStream_t stream) {
+  uint8_t* w = reinterpret_cast<uint8_t*>(workspace);
+  double* vals = reinterpret_cast<double*>(w);                     // [2][n]: means, vars
+  uint64_t* keys = reinterpret_cast<uint64_t*>(w + (size_t)n * 16);  // [2][n]
+  int* kept = reinterpret_cast<int*>(w + (size_t)n * 32);            // [2][n]
+  calib_stats_kernel<<<(n + 127) / 128, 128, 0, stream>>>(e, counts, n, ld, vals, vals + n);
+  int rc = check_launch("calibrate_stats");
+  if (rc) return rc;
+  calib_rank_kernel<<<2, kNT, 0, stream>>>(vals, n, rank, keys, kept, out);
+  return check_launch("calibrate_rank");
+}
 
 int launch_entropy_trigger(const ChessState& st, const Workspace& ws, const float* logits,
                            int64_t vocab, int64_t ld, const ChessTriggerCfg& cfg, double* out,

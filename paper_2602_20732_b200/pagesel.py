@@ -586,6 +586,36 @@ def calibrate(samples, percentile=0.99):
                              percentile, len(samples))
 
 
+def calibrate_device(entropies, counts=None, percentile=0.99, device=None):
+    """calibrate (uncertainty.py:59-83) from raw per-token entropy streams on
+    the device: page_uncertainty of every page (NumPy pairwise order, so the
+    statistics are bit-identical to the host ones) and the independent
+    nearest-rank percentiles, in two kernels.  entropies: [pages, n] (array or
+    tensor, f64); counts: entries per page (default n each).  Returns the same
+    TriggerThresholds as calibrate(page_uncertainty(...) per page)."""
+    e = torch.as_tensor(entropies, dtype=torch.float64, device=_device(device)).contiguous()
+    if e.dim() != 2 or e.shape[0] == 0:
+        raise CalibrationError("cannot calibrate on an empty sample")
+    if not 0.0 < percentile < 1.0:
+        raise CalibrationError(f"percentile must be in (0, 1), got {percentile}")
+    n_pages = int(e.shape[0])
+    if percentile >= 0.99 and n_pages < 100:
+        warnings.warn(f"only {n_pages} calibration pages for percentile {percentile}; "
+                      "thresholds will be coarse", stacklevel=2)
+    if counts is None:
+        c = torch.full((n_pages,), e.shape[1], dtype=torch.int32, device=e.device)
+    else:
+        c = torch.as_tensor(counts, dtype=torch.int32, device=e.device).contiguous()
+        if bool((c < 1).any()) or bool((c > e.shape[1]).any()):
+            raise ValueError("page has no generated tokens")
+    out = torch.empty(2, dtype=torch.float64, device=e.device)
+    ws = torch.empty(_lib.load().chess_calibrate_workspace_bytes(n_pages), dtype=torch.uint8, device=e.device)
+    _lib.call("chess_calibrate", _lib.ptr(e), _lib.ptr(c), n_pages, e.stride(0), float(percentile),
+              _lib.ptr(out), _lib.ptr(ws), _sp())
+    tau = out.cpu().tolist()
+    return TriggerThresholds(tau[0], tau[1], percentile, n_pages)
+
+
 def check_trigger(u, thresholds, mode="joint"):
     """Strict joint / any test (uncertainty.py:86-98)."""
     high_h = u.mean_entropy > thresholds.tau_entropy

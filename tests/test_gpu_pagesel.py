@@ -234,3 +234,34 @@ def test_decode_loop_matches_reference(run_idx):
     assert [s.recall for s in rep.steps] == run["recall"]
     assert rep.zero_copy_ok
     assert rep.summary()["trigger_count"] == run["summary"]["trigger_count"]
+
+
+def test_calibrate_device_golden_and_random():
+    """calibrate (uncertainty.py:59-83) on the device: bit-identical
+    thresholds against the reference's golden calibration (ragged pages) and
+    against the oracle on random streams, including heavy ties."""
+    from oracle import pagesel_ref as oref
+
+    doc = json.loads((GOLD / "uncertainty.json").read_text())
+    pages = doc["pages"]
+    n = max(len(pg["entropies"]) for pg in pages)
+    ent = np.zeros((len(pages), n))
+    for i, pg in enumerate(pages):
+        ent[i, : len(pg["entropies"])] = pg["entropies"]
+    counts = [len(pg["entropies"]) for pg in pages]
+    th = ps.calibrate_device(ent, counts, doc["calibration"]["percentile"])
+    assert (th.tau_entropy, th.tau_varentropy) == (doc["calibration"]["tau_H"], doc["calibration"]["tau_V"])
+    rng = np.random.default_rng(9)
+    for n_pages, B, p in ((1, 32, 0.5), (150, 32, 0.99), (1000, 16, 0.95), (4097, 32, 0.9), (300, 8, 0.3)):
+        ent = rng.gamma(2.0, 0.1, size=(n_pages, B))
+        if n_pages > 100:
+            ent[: n_pages // 3] = 0.25  # ties across pages
+        cnt = rng.integers(1, B + 1, size=n_pages)
+        stats = [oref.page_stats(ent[i, : cnt[i]]) for i in range(n_pages)]
+        want = oref.calibrate([s[0] for s in stats], [s[1] for s in stats], p)
+        got = ps.calibrate_device(ent, cnt, p)
+        assert (got.tau_entropy, got.tau_varentropy) == want, (n_pages, B, p)
+    with pytest.raises(ps.CalibrationError):
+        ps.calibrate_device(np.zeros((0, 4)))
+    with pytest.raises(ps.CalibrationError):
+        ps.calibrate_device(np.zeros((3, 4)), percentile=1.0)
