@@ -97,7 +97,10 @@ __device__ __forceinline__ void trace_max(int which) {
   if (kTrace) atomicMax(&s_trace[which], (unsigned long long)global_ns());
 }
 
-constexpr int kMaxCluster = 8;  // portable cluster size cap (inbox slots = cap - 1)
+// Cluster size cap (inbox slots = cap - 1).  Measured (profiles/r01/attn_micro/
+// sweep_cluster_cap.txt): b=1 ws16 4.3 us at 4 vs 5.3 at 8 (2-page pieces spend
+// more on merging than they save on streaming); b=4 8.6 at 4 vs 8.3 at 2.
+constexpr int kMaxCluster = 4;
 
 // XC: cluster-merge variant (piece mode with one segment per thread-block
 // cluster): the leader CTA owns an inbox for the other CTAs' piece states.
@@ -975,7 +978,8 @@ int cluster_size_for(int segs) {
   }
   static const bool off = getenv("CHESS_ATTN_CLUSTER") && atoi(getenv("CHESS_ATTN_CLUSTER")) == 0;  // A/B
   if (off || segs <= 0) return 0;
-  for (int cl = kMaxCluster; cl >= 2; cl /= 2)
+  static const int cl_cap = getenv("CHESS_ATTN_CLMAX") ? atoi(getenv("CHESS_ATTN_CLMAX")) : kMaxCluster;  // A/B
+  for (int cl = std::min(kMaxCluster, cl_cap); cl >= 2; cl /= 2)
     if (segs <= max_active[cl] && segs * cl <= num_sms()) return cl;
   return 0;
 }
