@@ -5,7 +5,7 @@
 set -u
 OUT=gpurun_out/${1:-prof}
 mkdir -p $OUT
-KREGEX='regex:sparse_decode|select_scan|append_kernel|seal_kernel|entropy|build_ws|reset_kernel'
+KREGEX='regex:sparse_decode|select_scan|append_kernel|seal_kernel|entropy|build_ws|flush_ws|reset_kernel'
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k "$KREGEX" --csv \
   --log-file $OUT/launches.csv python bench.py --steps 3 --warmup 3 --headline-only --no-cpu-baseline \
   > $OUT/launches_bench.log 2>&1
