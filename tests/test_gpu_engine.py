@@ -45,15 +45,15 @@ def _inputs(sh, tokens, seed):
     return k, v, q, lg
 
 
-@pytest.mark.parametrize("policy", ["always", "every_step"])
+@pytest.mark.parametrize("policy,full_scan", [("always", False), ("every_step", False), ("every_step", True)])
 @pytest.mark.parametrize("graph", [False, True])
-def test_concurrent_step_equals_sequential(policy, graph):
+def test_concurrent_step_equals_sequential(policy, full_scan, graph):
     cfg = preset_config("aggressive", page_size=B, pages_per_chunk=4, chunks_per_grid=4, window_pages=2)
     tokens = 2 * B + 5
     runs = []
     for concurrent in (False, True):
         st, n_ctx = _state(seed=1)
-        dec = ChessDecoder(st, cfg, policy=policy, concurrent_select=concurrent)
+        dec = ChessDecoder(st, cfg, policy=policy, concurrent_select=concurrent, full_scan=full_scan)
         dec.build_index(torch.full((3,), n_ctx, dtype=torch.int32, device="cuda"))
         dec.initial_selection()
         k, v, q, lg = _inputs(st.shape, tokens, seed=2)
