@@ -8,17 +8,20 @@
 //
 // B200 design — HBM-bound, one persistent CTA per SM:
 //  * work list = every (slot, kv head, working-set page) of the layer, laid
-//    out segment by segment (segment = one (slot, kv head)).  Piece mode
-//    (segments <= CTAs): each segment is cut into k = floor(G/segments)
-//    pieces of >= 4 pages, one per CTA (no merge when k = 1).  Stream-K
-//    (more segments): CTA c owns pages [c*N/G, (c+1)*N/G);
+//    out segment by segment (segment = one (slot, kv head)).  Three modes:
+//    cluster-merge (segments * 2 <= SMs: each segment split over a 2- or
+//    4-CTA thread-block cluster, peer states pushed into the leader's smem
+//    with st.async); piece (segments <= CTAs: k = floor(G/segments) pieces
+//    of >= 4 pages, no merge when k = 1 — cfg3); stream-K (more segments,
+//    two CTAs per SM: CTA c owns pages [c*N/G, (c+1)*N/G), split segments
+//    merged by the last CTA);
 //  * the last warp is the TMA producer: block-table ids of 32 pages come from
-//    one coalesced load (prefetched a batch ahead); pages go out in runs whose
-//    2-D tensor loads (128B swizzle, [64 cols x B rows] boxes) are issued by
-//    4 lanes per page in parallel into an S-stage ring of K+V page tiles; each
+//    one coalesced load (prefetched a batch ahead); pages go out in runs of
+//    3 whose 4-D tensor loads (128B swizzle, one box per K or V tile) are
+//    issued by lanes in parallel into an S-stage ring of K+V page tiles; each
 //    piece's GQA q rows go through a 2-slot q ring; the first run is issued
 //    before griddepcontrol.wait so it overlaps the previous kernel;
-//  * consumer warps take pages round-robin: S^T = K q^T and O^T += V^T P^T
+//  * 4 consumer warps take pages round-robin: S^T = K q^T and O^T += V^T P^T
 //    with mma.sync m16n8k16 (tokens as M; P^T via movmatrix, never in smem),
 //    online softmax per head in registers;
 //  * piece states are merged asynchronously by the last consumer warp to
