@@ -253,7 +253,7 @@ def run_gpu(args):
 
     def select_bytes(stats):
         # rows actually scanned: G + A_c + A_p per sequence, f32/f64 rows; + anchor
-        es = 4 if args.summary_dtype == "f32" else 8
+        es = {"f32": 4, "f64": 8, "bf16": 2}[args.summary_dtype]
         rows = stats[:, 0] + stats[:, 3] + stats[:, 4] if not args.full_scan else stats[:, 0] + stats[:, 1] + stats[:, 2]
         return float(np.sum(rows) * sh.dim * es + batch * sh.dim * 8)
 
@@ -389,7 +389,7 @@ def run_gpu(args):
         "higher_is_better": True,
         "scaling": "strong" if head else "weak",
         "vs_baseline": None,
-        "dtype": "bf16 KV / f32 summaries / f64 scores",
+        "dtype": f"bf16 KV / {args.summary_dtype} summaries / f64 scores",
         "data": "synthetic (planted-relevance keys, random-init shapes)",
         "config": {
             "workload": f"{cfg_name}: {DESCRIPTIONS[cfg_name]}",
@@ -564,7 +564,7 @@ def main():
     ap.add_argument("--impl", default="chess", choices=["chess", "reference"])
     ap.add_argument("--config", default="cfg3")
     ap.add_argument("--batch", type=int, default=None)
-    ap.add_argument("--summary-dtype", default="f32", choices=["f32", "f64"])
+    ap.add_argument("--summary-dtype", default="f32", choices=["f32", "f64", "bf16"])
     ap.add_argument("--full-scan", action="store_true")
     ap.add_argument("--headline-only", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -80,7 +80,8 @@ typedef struct ChessDims {
   int32_t max_pages;       /* per-sequence page-table / index capacity         */
   int32_t window_pages;    /* W   (config.py:33)                               */
   int32_t max_ws;          /* block-table row capacity                         */
-  int32_t summary_dtype;   /* 0: scan float32 mirrors, 1: scan float64         */
+  int32_t summary_dtype;   /* 0: scan float32 mirrors, 1: scan float64,
+                            * 2: scan bf16 mirrors (held in the *_vec32 buffers) */
   int64_t dim;             /* D                                                */
   int64_t ld;              /* summary row stride in elements (>= D, % 4 == 0)  */
   int64_t n_phys;          /* physical pages in the KV pool                    */

@@ -158,9 +158,11 @@ static int validate(const ChessDims& d) {
   if (d.dim != (int64_t)d.layers * d.kv_heads * d.head_dim)
     return fail(CHESS_ERR_CONFIG, "dim must equal layers*kv_heads*head_dim");
   if (d.ld < d.dim || d.ld % 4) return fail(CHESS_ERR_CONFIG, "ld must be >= dim and a multiple of 4");
+  if (d.summary_dtype == 2 && d.ld % 8)
+    return fail(CHESS_ERR_CONFIG, "bf16 summary mirrors need ld %% 8 == 0 (16-byte rows for the bulk copies)");
   if (d.max_pages < 1 || d.max_ws < 1) return fail(CHESS_ERR_CONFIG, "max_pages/max_ws must be >= 1");
   if (d.n_phys < 1) return fail(CHESS_ERR_CONFIG, "store capacity must be >= 1 page");
-  if (d.summary_dtype != 0 && d.summary_dtype != 1) return fail(CHESS_ERR_CONFIG, "summary_dtype must be 0 or 1");
+  if (d.summary_dtype < 0 || d.summary_dtype > 2) return fail(CHESS_ERR_CONFIG, "summary_dtype must be 0 (f32), 1 (f64) or 2 (bf16)");
   return CHESS_OK;
 }
 

@@ -42,7 +42,11 @@ __host__ __device__ inline int64_t max_rows(const ChessDims& d) { return d.max_p
 // bulk copy (f32 mirrors: 4096, f64 rows: 2048), so a ring of 12 stages
 // holds 1.5 items of 8 rows.
 constexpr int kScanSliceBytes = 16384;
-__host__ __device__ constexpr int scan_slice(int summary_dtype) { return summary_dtype == 0 ? kScanSliceBytes / 4 : kScanSliceBytes / 8; }
+// summary_dtype: 0 f32 mirrors, 1 f64 (no mirrors), 2 bf16 mirrors
+__host__ __device__ constexpr int summary_elem_bytes(int summary_dtype) {
+  return summary_dtype == 0 ? 4 : (summary_dtype == 1 ? 8 : 2);
+}
+__host__ __device__ constexpr int scan_slice(int summary_dtype) { return kScanSliceBytes / summary_elem_bytes(summary_dtype); }
 constexpr int kScanRows = 8;       // rows per work item
 constexpr int kScanThreads = 256;
 constexpr int kMaxBatch = 1024;
@@ -107,6 +111,13 @@ __device__ __forceinline__ float2 bf2x2f(uint32_t packed) {
   r.x = __uint_as_float(packed << 16);
   r.y = __uint_as_float(packed & 0xffff0000u);
   return r;
+}
+
+// write a scanned-summary mirror element (the *_vec32 buffers hold f32 rows
+// for summary_dtype 0 and bf16 rows for 2; f64 scans read the f64 rows)
+__device__ __forceinline__ void store_mirror(float* base, int64_t i, double v, int summary_dtype) {
+  if (summary_dtype == 0) base[i] = (float)v;
+  else if (summary_dtype == 2) reinterpret_cast<__nv_bfloat16*>(base)[i] = __double2bfloat16(v);
 }
 
 // Orderable key for f64 scores: larger score -> larger key.  -0.0 is
@@ -328,6 +339,11 @@ __device__ __forceinline__ void st_release_gpu(int* p, int v) {
 __device__ __forceinline__ float4 lds_f4(uint32_t a) {
   float4 v;
   asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ uint4 lds_u4(uint32_t a) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
   return v;
 }
 __device__ __forceinline__ double2 lds_d2(uint32_t a) {

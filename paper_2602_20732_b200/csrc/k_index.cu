@@ -285,11 +285,9 @@ __global__ void __launch_bounds__(kNT) seal_kernel(ChessState st, int32_t* done)
     const double cen_g = __ddiv_rn(o.gsum, (double)o.gcnt);
     st.chunk_vec64[((int64_t)s * mc + c) * ld + j] = cen_c;
     st.grid_vec64[((int64_t)s * mg + g) * ld + j] = cen_g;
-    if (d.summary_dtype == 0) {
-      st.page_vec32[((int64_t)s * d.max_pages + P) * ld + j] = (float)v;
-      st.chunk_vec32[((int64_t)s * mc + c) * ld + j] = (float)cen_c;
-      st.grid_vec32[((int64_t)s * mg + g) * ld + j] = (float)cen_g;
-    }
+    store_mirror(st.page_vec32, ((int64_t)s * d.max_pages + P) * ld + j, v, d.summary_dtype);
+    store_mirror(st.chunk_vec32, ((int64_t)s * mc + c) * ld + j, cen_c, d.summary_dtype);
+    store_mirror(st.grid_vec32, ((int64_t)s * mg + g) * ld + j, cen_g, d.summary_dtype);
     // Eq.3 anchor over the sealed pages (engine passes tail=None, simulate.py:136)
     st.anchor[(int64_t)s * ld + j] = anchor_elem(pv64, ld, P + 1, d.window_pages, j);
     ks[j] = 0.0;
@@ -357,11 +355,9 @@ __global__ void __launch_bounds__(kNT) fold_rows_kernel(ChessState st, int s, co
     const double cen_g = __ddiv_rn(o.gsum, (double)o.gcnt);
     st.chunk_vec64[((int64_t)s * mc + c) * ld + j] = cen_c;
     st.grid_vec64[((int64_t)s * mg + g) * ld + j] = cen_g;
-    if (d.summary_dtype == 0) {
-      st.page_vec32[((int64_t)s * d.max_pages + P) * ld + j] = (float)v;
-      st.chunk_vec32[((int64_t)s * mc + c) * ld + j] = (float)cen_c;
-      st.grid_vec32[((int64_t)s * mg + g) * ld + j] = (float)cen_g;
-    }
+    store_mirror(st.page_vec32, ((int64_t)s * d.max_pages + P) * ld + j, v, d.summary_dtype);
+    store_mirror(st.chunk_vec32, ((int64_t)s * mc + c) * ld + j, cen_c, d.summary_dtype);
+    store_mirror(st.grid_vec32, ((int64_t)s * mg + g) * ld + j, cen_g, d.summary_dtype);
     st.anchor[(int64_t)s * ld + j] = anchor_elem(pv64, ld, P + 1, d.window_pages, j);
   }
   __syncthreads();
@@ -438,7 +434,7 @@ __global__ void __launch_bounds__(kNT) build_kernel(ChessState st, const int32_t
       const int64_t j = j0 + q;
       if (j >= ld) break;
       pv64[(int64_t)p * ld + j] = v[q];
-      if (d.summary_dtype == 0) st.page_vec32[((int64_t)s * d.max_pages + p) * ld + j] = (float)v[q];
+      store_mirror(st.page_vec32, ((int64_t)s * d.max_pages + p) * ld + j, v[q], d.summary_dtype);
       const FoldOut o = fold_page(v[q], p, Nc, Ng, csum[q], gsum[q]);
       csum[q] = o.csum;
       gsum[q] = o.gsum;
@@ -447,13 +443,13 @@ __global__ void __launch_bounds__(kNT) build_kernel(ChessState st, const int32_t
         const double cen = __ddiv_rn(o.csum, (double)o.ccnt);
         st.chunk_sum64[((int64_t)s * mc + c) * ld + j] = o.csum;
         st.chunk_vec64[((int64_t)s * mc + c) * ld + j] = cen;
-        if (d.summary_dtype == 0) st.chunk_vec32[((int64_t)s * mc + c) * ld + j] = (float)cen;
+        store_mirror(st.chunk_vec32, ((int64_t)s * mc + c) * ld + j, cen, d.summary_dtype);
       }
       if (p + 1 == p_end) {
         const double gc = __ddiv_rn(o.gsum, (double)o.gcnt);
         st.grid_sum64[((int64_t)s * mg + g) * ld + j] = o.gsum;
         st.grid_vec64[((int64_t)s * mg + g) * ld + j] = gc;
-        if (d.summary_dtype == 0) st.grid_vec32[((int64_t)s * mg + g) * ld + j] = (float)gc;
+        store_mirror(st.grid_vec32, ((int64_t)s * mg + g) * ld + j, gc, d.summary_dtype);
       }
     }
   }
@@ -512,14 +508,14 @@ __global__ void __launch_bounds__(kNT) from_vectors_pages(ChessState st, int s, 
   for (int p = p0; p < p1; ++p) {
     const double v = j < d.dim ? rows[(int64_t)p * row_stride + j] : 0.0;
     pv64[(int64_t)p * ld + j] = v;
-    if (d.summary_dtype == 0) st.page_vec32[((int64_t)s * d.max_pages + p) * ld + j] = (float)v;
+    store_mirror(st.page_vec32, ((int64_t)s * d.max_pages + p) * ld + j, v, d.summary_dtype);
     acc = (p == p0) ? v : __dadd_rn(acc, v);
   }
   if (d.dim == 1 && p1 - p0 >= 8) acc = np_pairwise_sum(pv64 + (int64_t)p0 * ld + j, p1 - p0, (int)ld);
   const double cen = __ddiv_rn(acc, (double)(p1 - p0));
   st.chunk_sum64[((int64_t)s * mc + c) * ld + j] = acc;
   st.chunk_vec64[((int64_t)s * mc + c) * ld + j] = cen;
-  if (d.summary_dtype == 0) st.chunk_vec32[((int64_t)s * mc + c) * ld + j] = (float)cen;
+  store_mirror(st.chunk_vec32, ((int64_t)s * mc + c) * ld + j, cen, d.summary_dtype);
 }
 
 __global__ void __launch_bounds__(kNT) from_vectors_grids(ChessState st, int s, int n_chunks) {
@@ -538,7 +534,7 @@ __global__ void __launch_bounds__(kNT) from_vectors_grids(ChessState st, int s, 
   const double cen = __ddiv_rn(acc, (double)(c1 - c0));
   st.grid_sum64[((int64_t)s * mg + g) * ld + j] = acc;
   st.grid_vec64[((int64_t)s * mg + g) * ld + j] = cen;
-  if (d.summary_dtype == 0) st.grid_vec32[((int64_t)s * mg + g) * ld + j] = (float)cen;
+  store_mirror(st.grid_vec32, ((int64_t)s * mg + g) * ld + j, cen, d.summary_dtype);
 }
 
 // ---------------------------------------------------------------------------

@@ -101,6 +101,26 @@ __device__ __forceinline__ const double* level_row_ptr<double>(const ChessState&
   return st.page_vec64 + ((int64_t)s * d.max_pages + row) * d.ld;
 }
 
+template <>
+__device__ __forceinline__ const __nv_bfloat16* level_row_ptr<__nv_bfloat16>(
+    const ChessState& st, const Workspace& ws, int s, int level, int i, const LevelShape& sh) {
+  // bf16 mirrors live in the *_vec32 buffers (summary_dtype 2)
+  const ChessDims& d = st.d;
+  const int64_t mr = max_rows(d);
+  int which, row;
+  if (level == 3) {
+    which = i < sh.G ? 0 : (i < sh.G + sh.C ? 1 : 2);
+    row = which == 0 ? i : (which == 1 ? i - sh.G : i - sh.G - sh.C);
+  } else {
+    which = level;
+    row = level == 0 ? i : __ldcg(&ws.cand[((int64_t)s * 3 + level) * mr + i]);
+  }
+  const __nv_bfloat16* base = reinterpret_cast<const __nv_bfloat16*>(
+      which == 0 ? st.grid_vec32 : (which == 1 ? st.chunk_vec32 : st.page_vec32));
+  const int64_t rows = which == 0 ? max_grids(d) : (which == 1 ? max_chunks(d) : (int64_t)d.max_pages);
+  return base + ((int64_t)s * rows + row) * d.ld;
+}
+
 // ---------------------------------------------------------------------------
 // tail: reduce partials, top-k, emit next level (block-wide, one slot)
 // ---------------------------------------------------------------------------
@@ -317,6 +337,32 @@ struct ScanCfg {
   static constexpr int kGroups = kPerThread / kVec;                // chunks per thread
   __device__ static int off(int v) { return (v * kNT + (int)threadIdx.x) * kVec; }
 };
+
+// acc += a[kVec*v ..] . (16-byte chunk of the row at shared address ad), in f64
+template <typename T>
+__device__ __forceinline__ void fma_chunk(double& acc, const double* a, int v, uint32_t ad) {
+  constexpr int kVec = 16 / (int)sizeof(T);
+  if constexpr (sizeof(T) == 4) {
+    const float4 f = lds_f4(ad);
+    acc = __fma_rn(a[kVec * v + 0], (double)f.x, acc);
+    acc = __fma_rn(a[kVec * v + 1], (double)f.y, acc);
+    acc = __fma_rn(a[kVec * v + 2], (double)f.z, acc);
+    acc = __fma_rn(a[kVec * v + 3], (double)f.w, acc);
+  } else if constexpr (sizeof(T) == 8) {
+    const double2 f = lds_d2(ad);
+    acc = __fma_rn(a[kVec * v + 0], f.x, acc);
+    acc = __fma_rn(a[kVec * v + 1], f.y, acc);
+  } else {  // bf16 mirrors
+    const uint4 w = lds_u4(ad);
+    const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const float2 f = bf2x2f(ws[q]);
+      acc = __fma_rn(a[kVec * v + 2 * q], (double)f.x, acc);
+      acc = __fma_rn(a[kVec * v + 2 * q + 1], (double)f.y, acc);
+    }
+  }
+}
 
 template <typename T>
 __global__ void __launch_bounds__(kScanCTA, CHESS_SCAN_MINB) select_scan_kernel(ChessState st, Workspace ws,
@@ -555,18 +601,7 @@ __global__ void __launch_bounds__(kScanCTA, CHESS_SCAN_MINB) select_scan_kernel(
         for (int v = 0; v < SC::kGroups; ++v) {
 #pragma unroll
           for (int r = 0; r < kScanRows; ++r) {
-            const uint32_t ad = rowa[r] + (uint32_t)(SC::off(v) * sizeof(T));
-            if constexpr (sizeof(T) == 4) {
-              const float4 f = lds_f4(ad);
-              acc[r] = __fma_rn(a[4 * v + 0], (double)f.x, acc[r]);
-              acc[r] = __fma_rn(a[4 * v + 1], (double)f.y, acc[r]);
-              acc[r] = __fma_rn(a[4 * v + 2], (double)f.z, acc[r]);
-              acc[r] = __fma_rn(a[4 * v + 3], (double)f.w, acc[r]);
-            } else {
-              const double2 f = lds_d2(ad);
-              acc[r] = __fma_rn(a[2 * v + 0], f.x, acc[r]);
-              acc[r] = __fma_rn(a[2 * v + 1], f.y, acc[r]);
-            }
+            fma_chunk<T>(acc[r], a, v, rowa[r] + (uint32_t)(SC::off(v) * sizeof(T)));
           }
         }
       } else {
@@ -576,18 +611,7 @@ __global__ void __launch_bounds__(kScanCTA, CHESS_SCAN_MINB) select_scan_kernel(
 #pragma unroll
             for (int r = 0; r < kScanRows; ++r) {
               if (r < p.rows) {
-                const uint32_t ad = rowa[r] + (uint32_t)(SC::off(v) * sizeof(T));
-                if constexpr (sizeof(T) == 4) {
-                  const float4 f = lds_f4(ad);
-                  acc[r] = __fma_rn(a[4 * v + 0], (double)f.x, acc[r]);
-                  acc[r] = __fma_rn(a[4 * v + 1], (double)f.y, acc[r]);
-                  acc[r] = __fma_rn(a[4 * v + 2], (double)f.z, acc[r]);
-                  acc[r] = __fma_rn(a[4 * v + 3], (double)f.w, acc[r]);
-                } else {
-                  const double2 f = lds_d2(ad);
-                  acc[r] = __fma_rn(a[2 * v + 0], f.x, acc[r]);
-                  acc[r] = __fma_rn(a[2 * v + 1], f.y, acc[r]);
-                }
+                fma_chunk<T>(acc[r], a, v, rowa[r] + (uint32_t)(SC::off(v) * sizeof(T)));
               }
             }
           }
@@ -963,18 +987,7 @@ __global__ void __launch_bounds__(kScanCTA, 1) select_flow_kernel(ChessState st,
 #pragma unroll
           for (int r = 0; r < kScanRows; ++r) {
             if (r < x.rows) {
-              const uint32_t ad = rowa[r] + (uint32_t)(SC::off(v) * sizeof(T));
-              if constexpr (sizeof(T) == 4) {
-                const float4 f = lds_f4(ad);
-                acc[r] = __fma_rn(a[4 * v + 0], (double)f.x, acc[r]);
-                acc[r] = __fma_rn(a[4 * v + 1], (double)f.y, acc[r]);
-                acc[r] = __fma_rn(a[4 * v + 2], (double)f.z, acc[r]);
-                acc[r] = __fma_rn(a[4 * v + 3], (double)f.w, acc[r]);
-              } else {
-                const double2 f = lds_d2(ad);
-                acc[r] = __fma_rn(a[2 * v + 0], f.x, acc[r]);
-                acc[r] = __fma_rn(a[2 * v + 1], f.y, acc[r]);
-              }
+              fma_chunk<T>(acc[r], a, v, rowa[r] + (uint32_t)(SC::off(v) * sizeof(T)));
             }
           }
         }
@@ -1315,12 +1328,14 @@ int launch_select(const ChessState& st, const Workspace& ws, const SelParams& pr
   static const int flow_env = getenv("CHESS_SELECT_FLOW") ? atoi(getenv("CHESS_SELECT_FLOW")) : 0;
   if (flow_env && !prm.full_scan && !prm.xout && prm.mode == 0 && st.d.batch <= kFlowMaxBatch)
     return st.d.summary_dtype == 0 ? launch_flow<float>(st, ws, prm, stream)
-                                   : launch_flow<double>(st, ws, prm, stream);
+           : st.d.summary_dtype == 2 ? launch_flow<__nv_bfloat16>(st, ws, prm, stream)
+                                     : launch_flow<double>(st, ws, prm, stream);
   const int nlev = prm.full_scan ? 1 : 3;
   for (int li = 0; li < nlev; ++li) {
     const int level = prm.full_scan ? 3 : li;
-    const int rc = st.d.summary_dtype == 0 ? launch_scan<float>(st, ws, prm, level, stream)
-                                           : launch_scan<double>(st, ws, prm, level, stream);
+    const int rc = st.d.summary_dtype == 0   ? launch_scan<float>(st, ws, prm, level, stream)
+                   : st.d.summary_dtype == 2 ? launch_scan<__nv_bfloat16>(st, ws, prm, level, stream)
+                                             : launch_scan<double>(st, ws, prm, level, stream);
     if (rc) return rc;
   }
   return CHESS_OK;
@@ -1329,8 +1344,9 @@ int launch_select(const ChessState& st, const Workspace& ws, const SelParams& pr
 // head shard: the scan of one level with its tail exporting partial scores
 int launch_select_partial(const ChessState& st, const Workspace& ws, const SelParams& prm,
                           int level, cudaStream_t stream) {
-  return st.d.summary_dtype == 0 ? launch_scan<float>(st, ws, prm, level, stream)
-                                 : launch_scan<double>(st, ws, prm, level, stream);
+  return st.d.summary_dtype == 0   ? launch_scan<float>(st, ws, prm, level, stream)
+         : st.d.summary_dtype == 2 ? launch_scan<__nv_bfloat16>(st, ws, prm, level, stream)
+                                   : launch_scan<double>(st, ws, prm, level, stream);
 }
 
 int launch_select_combine(const ChessState& st, const Workspace& ws, const SelParams& prm,

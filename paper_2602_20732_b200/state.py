@@ -34,7 +34,7 @@ class Shape:
     window_pages: int
     max_ws: int
     n_phys: int
-    summary_dtype: str = "f32"  # "f32" mirrors scanned, or "f64"
+    summary_dtype: str = "f32"  # "f32" or "bf16" mirrors scanned, or "f64"
 
     @property
     def dim(self) -> int:
@@ -42,7 +42,8 @@ class Shape:
 
     @property
     def ld(self) -> int:
-        return _round_up(self.dim, 4)
+        # bf16 mirror rows must be 16-byte multiples for the scan's bulk copies
+        return _round_up(self.dim, 8 if self.summary_dtype == "bf16" else 4)
 
     @property
     def max_chunks(self) -> int:
@@ -83,10 +84,11 @@ class DecodeState:
         self.grid_sum64 = torch.zeros((b, s.max_grids, ld), **f64)
         self.chunk_vec64 = torch.zeros((b, s.max_chunks, ld), **f64)
         self.grid_vec64 = torch.zeros((b, s.max_grids, ld), **f64)
-        if s.summary_dtype == "f32":
-            self.page_vec32 = torch.zeros((b, s.max_pages, ld), **f32)
-            self.chunk_vec32 = torch.zeros((b, s.max_chunks, ld), **f32)
-            self.grid_vec32 = torch.zeros((b, s.max_grids, ld), **f32)
+        if s.summary_dtype in ("f32", "bf16"):
+            mdt = dict(f32) if s.summary_dtype == "f32" else dict(dtype=torch.bfloat16, device=dev)
+            self.page_vec32 = torch.zeros((b, s.max_pages, ld), **mdt)
+            self.chunk_vec32 = torch.zeros((b, s.max_chunks, ld), **mdt)
+            self.grid_vec32 = torch.zeros((b, s.max_grids, ld), **mdt)
         else:
             self.page_vec32 = self.chunk_vec32 = self.grid_vec32 = None
         self.key_sum = torch.zeros((b, ld), **f64)
@@ -119,7 +121,7 @@ class DecodeState:
         d.head_dim, d.page_size = s.head_dim, s.page_size
         d.pages_per_chunk, d.chunks_per_grid = s.pages_per_chunk, s.chunks_per_grid
         d.max_pages, d.window_pages, d.max_ws = s.max_pages, s.window_pages, s.max_ws
-        d.summary_dtype = 0 if s.summary_dtype == "f32" else 1
+        d.summary_dtype = {"f32": 0, "f64": 1, "bf16": 2}[s.summary_dtype]
         d.dim, d.ld, d.n_phys = s.dim, ld, s.n_phys
         lib = _lib.load()
         _lib.check(lib.chess_validate_dims(C.byref(d)), "validate_dims")
@@ -170,7 +172,7 @@ class DecodeState:
 
     def scan_matrices(self):
         """(grid, chunk, page) matrices the selection scan reads."""
-        if self.shape.summary_dtype == "f32":
+        if self.shape.summary_dtype in ("f32", "bf16"):
             return self.grid_vec32, self.chunk_vec32, self.page_vec32
         return self.grid_vec64, self.chunk_vec64, self.page_vec64
 

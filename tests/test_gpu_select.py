@@ -162,3 +162,46 @@ def test_select_gated_by_fire_and_empty():
     assert int(st.n_semantic[0]) > 0
     assert int(st.n_semantic[1]) == 0 and int(st.ws_len[1]) == 0  # not fired: untouched
     assert int(st.n_semantic[2]) == 0 and int(st.ws_len[2]) == 0
+
+
+def test_select_bf16_mirrors_kernel_isolated_and_certified():
+    """summary_dtype bf16: the scan streams bf16 mirrors of the f64 centroids
+    (half the f32 bytes).  Kernel-isolated: exact against the oracle fed the
+    same bf16 mirrors.  End to end against the f64 oracle: a differing
+    selection must be a certified near-tie under the bf16 storage bound
+    eps_i = 2^-8 * sum_k |a_k v_ik|."""
+    from helpers import index_state, load_vectors, read_selection, set_tables
+
+    rng = np.random.default_rng(8)
+    flips = 0
+    for P, dim, cfg in _instances(rng, 25):
+        st = index_state(2, dim, 720, cfg, summary_dtype="bf16")
+        hs = []
+        for slot in range(2):
+            rows = rng.standard_normal((P, dim))
+            load_vectors(st, slot, rows)
+            set_tables(st, slot, P, cfg.sink_pages)
+            hs.append(ref.Hierarchy.from_rows(rows, cfg.pages_per_chunk, cfg.chunks_per_grid))
+        _select(st, cfg=cfg)
+        for slot, h in enumerate(hs):
+            G, C, Pn = h.counts
+            mats = (
+                st.grid_vec32[slot, :G, :dim].double().cpu().numpy(),
+                st.chunk_vec32[slot, :C, :dim].double().cpu().numpy(),
+                st.page_vec32[slot, :Pn, :dim].double().cpu().numpy(),
+            )
+            # mirrors are the f64 centroids rounded to bf16 (8 significant bits:
+            # relative error <= 2^-8)
+            for m64, m16 in zip((h.grid_vectors, h.chunk_vectors, h.page_vectors), mats):
+                assert np.all(np.abs(m16 - m64) <= 2.0**-8 * np.abs(m64) + 1e-300)
+            sem = read_selection(st, slot)[0]
+            sel_iso, _, _ = _oracle_on(h, cfg, mats)
+            np.testing.assert_array_equal(sem, sel_iso)
+            sel64, _, _ = _oracle_on(h, cfg)
+            if not np.array_equal(sem, sel64):
+                flips += 1
+                a, _ = ref.anchor(h.page_vectors, cfg.window_pages)
+                for mat64, mat16 in zip((h.grid_vectors, h.chunk_vectors, h.page_vectors), mats):
+                    bound = 2.0**-8 * (np.abs(mat64) @ np.abs(a))
+                    assert np.all(np.abs(mat64 @ a - mat16 @ a) <= bound)
+    assert flips <= 8
