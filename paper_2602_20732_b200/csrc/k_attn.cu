@@ -57,6 +57,15 @@ namespace {
 #ifndef CHESS_ATTN_RUN
 #define CHESS_ATTN_RUN 3
 #endif
+// q fragments: when a cluster-mode CTA's whole piece fits in the ring, its
+// consumers read q from global right after their own griddepcontrol.wait
+// (b=1 layer 4.25 -> 3.8 us).  Otherwise the producer's 2-slot smem q ring
+// stays: it also holds the producer's K/V run-ahead behind the PDL wait
+// (direct q for long pieces: cfg3 18.3 -> 20.4 us, cfg5 13.0 -> 13.8 us;
+// profiles/r01/attn_micro/sweep_qdirect.txt).
+#ifndef CHESS_ATTN_QDIRECT
+#define CHESS_ATTN_QDIRECT 1
+#endif
 constexpr int kConsumers = CHESS_ATTN_CONSUMERS;
 constexpr int kMaxCtasPerSm = 2;
 constexpr int kAttnMaxBatch = 256;  // per-slot tables live in smem
@@ -402,6 +411,7 @@ __global__ void __launch_bounds__(kThreads, CPS)
     u_end = (int)((int64_t)(c + 1) * N / G);
   }
 
+  const bool qdirect = CHESS_ATTN_QDIRECT && XC && (u_end - u_begin) <= C::kStages;
   // global page index u -> (slot, head, page within segment)
   auto locate = [&](int u, int& s, int& h, int& p) {
     int lo = 0, hi = nb;
@@ -477,7 +487,7 @@ __global__ void __launch_bounds__(kThreads, CPS)
         };
         // the kernel's first q load waits for the previous grid (PDL); the
         // first run of K/V pages is issued before it so it overlaps that wait
-        if (((starts >> c0) & 1u) && !first_run) issue_q(c0);
+        if (!qdirect && ((starts >> c0) & 1u) && !first_run) issue_q(c0);
         const int pg = lane >> 2, bx = lane & 3;
         const int i = c0 + pg;
         const int row0 = __shfl_sync(0xffffffffu, cur_row, min(i, 31));
@@ -497,7 +507,7 @@ __global__ void __launch_bounds__(kThreads, CPS)
         }
         __syncwarp();
         if (lane == 0) st_release_cta(&ctr[0], base + c1);
-        if (first_run) issue_q(0);
+        if (!qdirect && first_run) issue_q(0);
         c0 = c1;
       }
       cur_row = nxt_row;
@@ -531,7 +541,16 @@ __global__ void __launch_bounds__(kThreads, CPS)
 
     // q^T B-fragments from the q ring: b[ks][0] = q[g][16ks+2t..], b[ks][1] = q[g][16ks+8+2t..]
     uint32_t qb[C::kKS][2];
-    if (piece_n > 0) {
+    if (qdirect && piece_n > 0) {
+      if (k == 0 && args.mode != 8) pdl_wait();  // q comes from the previous grid
+      const uint32_t* qrow = reinterpret_cast<const uint32_t*>(
+          args.q + (int64_t)s * args.q_stride + ((int64_t)h * GQ + (g < GQ ? g : 0)) * HD);
+#pragma unroll
+      for (int ks = 0; ks < C::kKS; ++ks) {
+        qb[ks][0] = g < GQ ? __ldg(qrow + (ks * 16 + 2 * t) / 2) : 0u;
+        qb[ks][1] = g < GQ ? __ldg(qrow + (ks * 16 + 8 + 2 * t) / 2) : 0u;
+      }
+    } else if (piece_n > 0) {
       const int qs = k & 1;
       mbar_wait(&qfull[qs], (uint32_t)((k >> 1) & 1));
       const uint8_t* qrow = qbuf + qs * C::kQBytes + g * HD * 2;
