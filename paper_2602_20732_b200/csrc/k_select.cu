@@ -338,6 +338,10 @@ struct ScanCfg {
   __device__ static int off(int v) { return (v * kNT + (int)threadIdx.x) * kVec; }
 };
 
+__device__ __forceinline__ float to_f(float x) { return x; }
+__device__ __forceinline__ double to_f(double x) { return x; }
+__device__ __forceinline__ float to_f(__nv_bfloat16 x) { return bf2f(x); }
+
 // acc += a[kVec*v ..] . (16-byte chunk of the row at shared address ad), in f64
 template <typename T>
 __device__ __forceinline__ void fma_chunk(double& acc, const double* a, int v, uint32_t ad) {
@@ -691,6 +695,7 @@ __global__ void __launch_bounds__(kScanCTA, CHESS_SCAN_MINB) select_scan_kernel(
 // Deadlock freedom: items are grabbed in level order and a tail depends only
 // on items of its own level, which never wait on later levels.
 // ---------------------------------------------------------------------------
+constexpr int kSmallRowBytes = 16384;  // rows up to this size use select_small_kernel
 constexpr int kDescRing = 8;
 constexpr int kFlowMaxBatch = 256;  // per-slot scheduler tables live in shared memory
 constexpr int kDescEnd = -1, kDescFlush = -2;
@@ -1038,6 +1043,55 @@ __global__ void __launch_bounds__(kScanCTA, 1) select_flow_kernel(ChessState st,
 }
 
 // ---------------------------------------------------------------------------
+// Small-index cascade: one CTA per slot runs all three levels (no inter-CTA
+// hand-offs).  For short summary rows (<= 16 KB: the reference's CPU-demo
+// shape, D = 1024) the per-level launches, cross-CTA partial reductions and
+// tails of the streaming kernel cost far more than the bytes; here each warp
+// scores whole rows (lanes stride the row, fixed shuffle tree in f64) and the
+// same select_tail_topk runs between levels.
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void __launch_bounds__(kNT) select_small_kernel(ChessState st, Workspace ws, SelParams prm) {
+  __shared__ TailSmem sm;
+  const int s = blockIdx.x;
+  if (!fired(st, prm, s)) return;
+  const ChessDims& d = st.d;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const LevelShape sh = shape_of(st, s);
+  if (sh.P == 0) {  // as handle_empty_slots, for this slot
+    if (threadIdx.x == 0) {
+      st.n_semantic[s] = 0;
+      ws.cand_n[4 * s + 1] = 0;
+      ws.cand_n[4 * s + 2] = 0;
+      for (int i = 0; i < 8; ++i) st.sel_stats[8 * s + i] = 0;
+    }
+    block_sync<kNT>();
+    if (prm.defer_ws) {
+      if (threadIdx.x == 0) ws.ws_pending[s] = 1;
+    } else {
+      block_build_ws<kNT>(st, s, sm.scratch);
+    }
+    return;
+  }
+  const double* anc = st.anchor + (int64_t)s * d.ld;
+  double* sc = ws.scores + (int64_t)s * max_rows(d);
+  for (int level = 0; level < 3; ++level) {
+    const int n = level == 0 ? sh.G : ws.cand_n[4 * s + level];
+    for (int i = warp; i < n; i += kNT / 32) {
+      const T* row = level_row_ptr<T>(st, ws, s, level, i, sh);
+      double acc = 0.0;
+      for (int64_t j = lane; j < d.dim; j += 32) acc = __fma_rn(anc[j], (double)to_f(row[j]), acc);
+#pragma unroll
+      for (int o = 16; o >= 1; o >>= 1) acc += shfl_xor_d(acc, o);
+      if (lane == 0) sc[i] = acc;
+    }
+    block_sync<kNT>();
+    select_tail_topk(st, ws, prm, s, level, n, sm);
+    block_sync<kNT>();
+  }
+}
+
+// ---------------------------------------------------------------------------
 // KV-head shard: finish one level from every rank's exported
 // partial scores.  gathered = [world][batch][xld] (rank-major, the layout of
 // an all-gather of each rank's xout); the partials are added in rank order so
@@ -1330,6 +1384,18 @@ int launch_select(const ChessState& st, const Workspace& ws, const SelParams& pr
     return st.d.summary_dtype == 0 ? launch_flow<float>(st, ws, prm, stream)
            : st.d.summary_dtype == 2 ? launch_flow<__nv_bfloat16>(st, ws, prm, stream)
                                      : launch_flow<double>(st, ws, prm, stream);
+  // short rows: the whole cascade of a slot in one CTA (CHESS_SELECT_SMALL=0 to A/B)
+  static const int small_env = getenv("CHESS_SELECT_SMALL") ? atoi(getenv("CHESS_SELECT_SMALL")) : 1;
+  if (small_env && !prm.full_scan && !prm.xout && prm.mode == 0 &&
+      st.d.ld * summary_elem_bytes(st.d.summary_dtype) <= kSmallRowBytes) {
+    if (st.d.summary_dtype == 0)
+      select_small_kernel<float><<<st.d.batch, kNT, 0, stream>>>(st, ws, prm);
+    else if (st.d.summary_dtype == 2)
+      select_small_kernel<__nv_bfloat16><<<st.d.batch, kNT, 0, stream>>>(st, ws, prm);
+    else
+      select_small_kernel<double><<<st.d.batch, kNT, 0, stream>>>(st, ws, prm);
+    return check_launch("select_small");
+  }
   const int nlev = prm.full_scan ? 1 : 3;
   for (int li = 0; li < nlev; ++li) {
     const int level = prm.full_scan ? 3 : li;

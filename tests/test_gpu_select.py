@@ -8,6 +8,7 @@ to certified near-ties (end-to-end).
 """
 
 import math
+import os
 
 import numpy as np
 import pytest
@@ -205,3 +206,20 @@ def test_select_bf16_mirrors_kernel_isolated_and_certified():
                     bound = 2.0**-8 * (np.abs(mat64) @ np.abs(a))
                     assert np.all(np.abs(mat64 @ a - mat16 @ a) <= bound)
     assert flips <= 8
+
+
+@pytest.mark.skipif(os.environ.get("CHESS_SELECT_SMALL") == "0", reason="already the streaming path")
+def test_streaming_kernel_path_in_subprocess():
+    """The test shapes above have short rows, so they run the one-CTA-per-slot
+    cascade (select_small_kernel).  Re-run this module with that path off so
+    the streaming scan kernel (the one the model shapes use) passes the same
+    parity tests."""
+    import subprocess
+    import sys
+
+    env = dict(os.environ, CHESS_SELECT_SMALL="0")
+    here = os.path.dirname(os.path.abspath(__file__))
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider",
+                        os.path.join(here, "test_gpu_select.py")], env=env, capture_output=True, text=True,
+                       cwd=os.path.dirname(here), timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
