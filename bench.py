@@ -525,6 +525,9 @@ def cpu_baseline(cfg_name, steps=1):
     }
 
 
+REF_BUDGET_S = 90.0
+
+
 def run_reference(args):
     rank, world, _ = _dist_env()
     if rank != 0:
@@ -536,13 +539,20 @@ def run_reference(args):
     with limits:
         for _ in range(min(args.warmup, 1)):
             _cpu_step(*setup)
+        # K steps, but the CPU arm stops timing after REF_BUDGET_S seconds so a
+        # large --steps still finishes in minutes (the per-step mean is kept)
         t = time.perf_counter()
+        timed = 0
         for _ in range(args.steps):
             _cpu_step(*setup)
-        dt = (time.perf_counter() - t) / args.steps
+            timed += 1
+            if time.perf_counter() - t > REF_BUDGET_S:
+                break
+        dt = (time.perf_counter() - t) / timed
     v = 1.0 / dt
     sample = (f"each step = 1 sequence x 1 decode token of {args.config} (oracle NumPy port of "
-              f"pagesel selection + attention restatement + entropy)")
+              f"pagesel selection + attention restatement + entropy); {timed} of {args.steps} "
+              f"steps timed (budget {REF_BUDGET_S:.0f} s)")
     print(json.dumps({
         "impl": "reference",
         "metric": "decode tokens/s (select+attn every step) at 1% KV",
