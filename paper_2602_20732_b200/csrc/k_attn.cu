@@ -706,6 +706,69 @@ __global__ void __launch_bounds__(kThreads, CPS)
       }
     }
     __syncwarp();
+    if constexpr (XC && C::kEPL % (2 * kConsumers) == 0) {
+      // Cluster mode holds one piece per CTA, so every consumer warp is here:
+      // instead of one warp merging all four states, each merges a quarter
+      // of the (head, d) elements, pushes it to the leader (or, in the
+      // leader, waits for the peers' quarters and writes the output).
+      consumer_sync();
+      constexpr int kQ = GQ * HD / kConsumers, kE = kQ / 32;
+      const int e0 = warp * kQ + lane * kE;
+      const int hh = e0 / HD, el = e0 % HD;
+      float M = -INFINITY, L = 0.f, acc[kE];
+#pragma unroll
+      for (int e = 0; e < kE; ++e) acc[e] = 0.f;
+#pragma unroll
+      for (int w = 0; w < kConsumers; ++w) M = fmaxf(M, stv[(w * GQ + hh) * C::kRow + HD]);
+#pragma unroll
+      for (int w = 0; w < kConsumers; ++w) {
+        const float* pr = stv + (w * GQ + hh) * C::kRow;
+        const float f = pr[HD] == -INFINITY ? 0.f : exp2f(pr[HD] - M);
+        L = fmaf(pr[HD + 1], f, L);
+#pragma unroll
+        for (int e = 0; e < kE; e += 2) {
+          const float2 x = *reinterpret_cast<const float2*>(pr + el + e);
+          acc[e] = fmaf(x.x, f, acc[e]);
+          acc[e + 1] = fmaf(x.y, f, acc[e + 1]);
+        }
+      }
+      const int cr = c % args.cl;
+      if (cr != 0) {
+        const uint32_t rx = mapa_shared(smem_u32(xst + ((cr - 1) * GQ + hh) * C::kRow), 0);
+        const uint32_t rb = mapa_shared(smem_u32(xbar), 0);
+#pragma unroll
+        for (int e = 0; e < kE; e += 2) st_async_f32x2(rx + (uint32_t)(el + e) * 4u, acc[e], acc[e + 1], rb);
+        if (el == 0) st_async_f32x2(rx + (uint32_t)HD * 4u, M, L, rb);
+      } else {
+        mbar_wait_cluster(xbar, 0);
+        float Mx = M;
+        for (int r = 1; r < args.cl; ++r) Mx = fmaxf(Mx, xst[((r - 1) * GQ + hh) * C::kRow + HD]);
+        const float f0 = M == -INFINITY ? 0.f : exp2f(M - Mx);
+        float Lx = L * f0;
+#pragma unroll
+        for (int e = 0; e < kE; ++e) acc[e] *= f0;
+        for (int r = 1; r < args.cl; ++r) {
+          const float* pr = xst + ((r - 1) * GQ + hh) * C::kRow;
+          const float f = pr[HD] == -INFINITY ? 0.f : exp2f(pr[HD] - Mx);
+          Lx = fmaf(pr[HD + 1], f, Lx);
+#pragma unroll
+          for (int e = 0; e < kE; e += 2) {
+            const float2 x = *reinterpret_cast<const float2*>(pr + el + e);
+            acc[e] = fmaf(x.x, f, acc[e]);
+            acc[e + 1] = fmaf(x.y, f, acc[e + 1]);
+          }
+        }
+        const float inv = 1.f / Lx;
+        __nv_bfloat16* orow = args.out + (int64_t)s * args.out_stride + ((int64_t)h * GQ + hh) * HD + el;
+#pragma unroll
+        for (int e = 0; e < kE; e += 2)
+          *reinterpret_cast<__nv_bfloat162*>(orow + e) = __floats2bfloat162_rn(acc[e] * inv, acc[e + 1] * inv);
+        if (args.lse && el == 0) args.lse[(int64_t)s * d.q_heads + h * GQ + hh] = (Mx + log2f(Lx)) * kLn2;
+      }
+      u = piece_end;
+      ++k;
+      continue;
+    }
     int last = 0;
     if (lane == 0) {
       __threadfence_block();
