@@ -706,11 +706,14 @@ __global__ void __launch_bounds__(kThreads, CPS)
       }
     }
     __syncwarp();
-    if constexpr (XC && C::kEPL % (2 * kConsumers) == 0) {
-      // Cluster mode holds one piece per CTA, so every consumer warp is here:
-      // instead of one warp merging all four states, each merges a quarter
-      // of the (head, d) elements, pushes it to the leader (or, in the
-      // leader, waits for the peers' quarters and writes the output).
+    // A CTA whose range is exactly one piece (cluster mode; piece mode with
+    // one whole segment per CTA, as cfg3) has every consumer warp here and
+    // nothing left to stream: instead of one warp merging all four states,
+    // each merges a quarter of the (head, d) elements and writes it (piece
+    // mode), or pushes it to the cluster leader (whose warps then finish
+    // their quarters over the peers' states).
+    const bool one_piece = XC || (u_begin == seg_begin && u_end == seg_end);
+    if constexpr (C::kEPL % (2 * kConsumers) == 0) if (one_piece) {
       consumer_sync();
       constexpr int kQ = GQ * HD / kConsumers, kE = kQ / 32;
       const int e0 = warp * kQ + lane * kE;
@@ -732,22 +735,23 @@ __global__ void __launch_bounds__(kThreads, CPS)
           acc[e + 1] = fmaf(x.y, f, acc[e + 1]);
         }
       }
-      const int cr = c % args.cl;
-      if (cr != 0) {
+      const int cr = XC ? c % args.cl : 0;
+      if (XC && cr != 0) {
         const uint32_t rx = mapa_shared(smem_u32(xst + ((cr - 1) * GQ + hh) * C::kRow), 0);
         const uint32_t rb = mapa_shared(smem_u32(xbar), 0);
 #pragma unroll
         for (int e = 0; e < kE; e += 2) st_async_f32x2(rx + (uint32_t)(el + e) * 4u, acc[e], acc[e + 1], rb);
         if (el == 0) st_async_f32x2(rx + (uint32_t)HD * 4u, M, L, rb);
       } else {
-        mbar_wait_cluster(xbar, 0);
+        const int ncl = XC ? args.cl : 1;
+        if (XC) mbar_wait_cluster(xbar, 0);
         float Mx = M;
-        for (int r = 1; r < args.cl; ++r) Mx = fmaxf(Mx, xst[((r - 1) * GQ + hh) * C::kRow + HD]);
+        for (int r = 1; r < ncl; ++r) Mx = fmaxf(Mx, xst[((r - 1) * GQ + hh) * C::kRow + HD]);
         const float f0 = M == -INFINITY ? 0.f : exp2f(M - Mx);
         float Lx = L * f0;
 #pragma unroll
         for (int e = 0; e < kE; ++e) acc[e] *= f0;
-        for (int r = 1; r < args.cl; ++r) {
+        for (int r = 1; r < ncl; ++r) {
           const float* pr = xst + ((r - 1) * GQ + hh) * C::kRow;
           const float f = pr[HD] == -INFINITY ? 0.f : exp2f(pr[HD] - Mx);
           Lx = fmaf(pr[HD + 1], f, Lx);
