@@ -208,18 +208,20 @@ def test_select_bf16_mirrors_kernel_isolated_and_certified():
     assert flips <= 8
 
 
-@pytest.mark.skipif(os.environ.get("CHESS_SELECT_SMALL") == "0", reason="already the streaming path")
-def test_streaming_kernel_path_in_subprocess():
+@pytest.mark.skipif(os.environ.get("CHESS_SELECT_SMALL") == "0" or os.environ.get("CHESS_SELECT_FLOW") == "1",
+                    reason="already an alternate path")
+@pytest.mark.parametrize("env", [{"CHESS_SELECT_SMALL": "0"}, {"CHESS_SELECT_FLOW": "1"}],
+                         ids=["streaming", "dataflow"])
+def test_alternate_select_paths_in_subprocess(env):
     """The test shapes above have short rows, so they run the one-CTA-per-slot
-    cascade (select_small_kernel).  Re-run this module with that path off so
-    the streaming scan kernel (the one the model shapes use) passes the same
-    parity tests."""
+    cascade (select_small_kernel).  Re-run this module with that path off (the
+    streaming scan kernel the model shapes use) and with the opt-in dataflow
+    cascade, so both pass the same parity tests."""
     import subprocess
     import sys
 
-    env = dict(os.environ, CHESS_SELECT_SMALL="0")
     here = os.path.dirname(os.path.abspath(__file__))
     r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider",
-                        os.path.join(here, "test_gpu_select.py")], env=env, capture_output=True, text=True,
-                       cwd=os.path.dirname(here), timeout=900)
+                        os.path.join(here, "test_gpu_select.py")], env=dict(os.environ, **env),
+                       capture_output=True, text=True, cwd=os.path.dirname(here), timeout=900)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
