@@ -225,3 +225,31 @@ def test_alternate_select_paths_in_subprocess(env):
                         os.path.join(here, "test_gpu_select.py")], env=dict(os.environ, **env),
                        capture_output=True, text=True, cwd=os.path.dirname(here), timeout=900)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+
+
+def test_select_model_dimension_streaming_path():
+    """Parity at the model's flattened key dimension (Llama-3-8B: D = 32 x 8 x
+    128 = 32768, 128 KB f32 rows — the streaming scan kernel's regime) on a
+    2048-page index with a planted cluster: exact against the oracle fed the
+    same f32 mirrors, and equal to the f64 oracle."""
+    from helpers import index_state, load_vectors, read_selection, set_tables
+
+    rng = np.random.default_rng(21)
+    P, D = 2048, 32768
+    cfg = preset_config("aggressive")
+    rows = rng.standard_normal((P, D)).astype(np.float64) / np.sqrt(D)
+    sig = rng.standard_normal(D) / np.sqrt(D)
+    rows[640:660] += 4.0 * sig  # 1% planted relevance, chunk-aligned start
+    rows[-4:] += 2.0 * sig      # the window (anchor) carries the signal
+    st = index_state(1, D, P + 8, cfg, summary_dtype="f32")
+    load_vectors(st, 0, rows)
+    set_tables(st, 0, P, cfg.sink_pages)
+    _select(st, cfg=cfg)
+    h = ref.Hierarchy.from_rows(rows, cfg.pages_per_chunk, cfg.chunks_per_grid)
+    G, C, Pn = h.counts
+    mats = (st.grid_vec32[0, :G, :D].double().cpu().numpy(), st.chunk_vec32[0, :C, :D].double().cpu().numpy(),
+            st.page_vec32[0, :Pn, :D].double().cpu().numpy())
+    sem = read_selection(st, 0)[0]
+    np.testing.assert_array_equal(sem, _oracle_on(h, cfg, mats)[0])
+    np.testing.assert_array_equal(sem, _oracle_on(h, cfg)[0])
+    assert set(range(640, 660)) <= set(sem.tolist())  # the planted pages are found
