@@ -136,6 +136,26 @@ class ChessDecoder:
         """K1b: index pages [0, n_pages[s]) of every slot (prefill)."""
         _lib.call("chess_summary_build", self.state.ref, _lib.ptr(n_pages), _lib.stream_ptr(stream))
 
+    # ------------------------------------------------------------------
+    # continuous batching: slot eviction / admission (device page pool)
+    # ------------------------------------------------------------------
+    def evict(self, mask, stream=None):
+        """Finish the sequences in `mask` (u8 [batch]): their pool pages go
+        back to the free list and the slots are reset (kv_store.py:103-136)."""
+        st = self.state
+        if st.pool_free is not None:
+            st.pool_release(mask, stream)
+        st.reset(mask, stream)
+
+    def admit(self, mask, stream=None):
+        """Open fresh sequences in the (reset) slots of `mask`: reserve each
+        one's first page from the pool; tokens then enter through step()."""
+        st = self.state
+        counts = mask.to(torch.int32)
+        if st.pool_free is not None:
+            st.pool_reserve(counts, stream)
+        st.sink_count.masked_fill_(mask.bool(), self.config.sink_pages)
+
     def select(self, force_all=False, stream=None, defer_ws=False):
         if defer_ws:
             cfg = self.sel_cfg_all_defer if force_all else self.sel_cfg_defer

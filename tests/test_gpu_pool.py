@@ -181,3 +181,67 @@ def test_pool_requires_pool_buffers():
     st = DecodeState(_shape())
     with pytest.raises(Exception):
         st.pool_init()
+
+
+def test_evict_and_admit_reuses_slot_and_pages():
+    """Continuous batching on the device pool: finish slot 0 mid-run, admit a
+    new sequence into it and keep decoding slot 1.  The new sequence equals a
+    fresh single-sequence run fed the same tokens (summaries, selections and
+    working sets bit for bit, attention within the bf16 bound), slot 1 is
+    untouched by the turnover, and the evicted pages are reused."""
+    from oracle import attention as attn_ref
+
+    sh = _shape(batch=2, n_phys=40)
+    cfg = _cfg()
+    t1, t2 = 2 * B + 3, 3 * B + 2
+    k1, v1, q1, lg1 = _inputs(sh, t1, seed=4)
+    k2, v2, q2, lg2 = _inputs(sh, t2, seed=5)
+    st = DecodeState(sh, page_pool=True)
+    st.reset()
+    st.pool_init()
+    dec = ChessDecoder(st, cfg, policy="always")
+    dec.admit(torch.ones(2, dtype=torch.uint8, device="cuda"))
+    out = torch.zeros((sh.batch, sh.layers, sh.q_heads, sh.head_dim), device="cuda", dtype=torch.bfloat16)
+    for t in range(t1):
+        dec.step(k1[t], v1[t], q1[t], lg1[t], out)
+    torch.cuda.synchronize()
+    old_pages = set(st.page_table[0, : int(st.pool_end[0])].tolist())
+    slot1_before = st.page_vec64[1].clone()
+    m0 = torch.tensor([1, 0], dtype=torch.uint8, device="cuda")
+    dec.evict(m0)
+    dec.admit(m0)
+    outs = torch.zeros((t2,) + out.shape, device="cuda", dtype=torch.bfloat16)
+    for t in range(t2):
+        dec.step(k2[t], v2[t], q2[t], lg2[t], outs[t])
+    torch.cuda.synchronize()
+    st.check_pool()
+    new_pages = set(st.page_table[0, : int(st.pool_end[0])].tolist())
+    assert new_pages & old_pages  # the freed pages came back to slot 0
+    n1 = int(st.num_sealed[1])
+    # slot 1's earlier pages did not change across the turnover
+    n1_before = (t1 // B)
+    assert torch.equal(st.page_vec64[1, :n1_before], slot1_before[:n1_before])
+    assert n1 == (t1 + t2) // B
+
+    # reference: the same tokens as a fresh single sequence
+    sh1 = _shape(batch=1, n_phys=40)
+    ref_st = DecodeState(sh1, page_pool=True)
+    ref_st.reset()
+    ref_st.pool_init()
+    rdec = ChessDecoder(ref_st, cfg, policy="always")
+    rdec.admit(torch.ones(1, dtype=torch.uint8, device="cuda"))
+    routs = torch.zeros((t2, 1) + out.shape[1:], device="cuda", dtype=torch.bfloat16)
+    for t in range(t2):
+        rdec.step(k2[t][:1], v2[t][:1], q2[t][:1], lg2[t][:1], routs[t])
+    torch.cuda.synchronize()
+    for name in ("num_pages", "tail_fill", "num_sealed", "n_semantic", "ws_len"):
+        assert int(getattr(st, name)[0]) == int(getattr(ref_st, name)[0]), name
+    n = int(ref_st.num_sealed[0])
+    assert torch.equal(st.page_vec64[0, :n], ref_st.page_vec64[0, :n])
+    assert torch.equal(st.anchor[0], ref_st.anchor[0])
+    assert torch.equal(st.semantic[0, : int(st.n_semantic[0])], ref_st.semantic[0, : int(ref_st.n_semantic[0])])
+    assert torch.equal(st.ws_logical[0, : int(st.ws_len[0])], ref_st.ws_logical[0, : int(ref_st.ws_len[0])])
+    assert torch.equal(_logical_keys(st, 0), _logical_keys(ref_st, 0))
+    # attention: same math, possibly a different work split across CTAs
+    a, b_ = outs[:, 0].float(), routs[:, 0].float()
+    assert torch.all((a - b_).abs() <= 2.0**-7 * (b_.abs() + 2.0**-4)), (a - b_).abs().max()
