@@ -165,11 +165,14 @@ def run_gpu(args):
     P, B, L = wl.P, wl.B, sh.layers
     exchange = None
     if head:
-        from paper_2602_20732_b200.parallel import HeadShard, HeadShardExchange
+        from paper_2602_20732_b200.parallel import HeadShard, HeadShardExchange, PeerScoreExchange
 
         hs = HeadShard(rank, world, L, c["kv_heads"], c["q_heads"], c["head_dim"])
-        exchange = HeadShardExchange(hs, batch, sh.max_pages, sh.pages_per_chunk, sh.chunks_per_grid,
-                                     torch.device("cuda", local), full_scan=args.full_scan)
+        xcls = PeerScoreExchange if args.transport == "p2p" else HeadShardExchange
+        exchange = xcls(hs, batch, sh.max_pages, sh.pages_per_chunk, sh.chunks_per_grid,
+                        torch.device("cuda", local), full_scan=args.full_scan)
+        if args.transport == "p2p":
+            exchange.connect()  # IPC handles over the default group
     # sequences the whole job advances per step
     job_batch = batch if head else world * batch
 
@@ -399,8 +402,10 @@ def run_gpu(args):
             "preset": "aggressive (0.5, 0.2, 0.1), W=4, sinks=1",
             "parallelism": ("single GPU" if world == 1 and shard == "replica" else
                             {"batch": f"batch-shard x{world} (no data-path collective)",
-                             "head": f"kv-head-shard x{world} (NCCL: per-level partial-score "
-                                     f"all-gather + per-layer output all-gather)",
+                             "head": f"kv-head-shard x{world} (per-level partial-score exchange: "
+                                     + ("peer-memory stores fused into the scan tail"
+                                        if args.transport == "p2p" else "NCCL all-gather")
+                                     + "; per-layer output all-gather: NCCL)",
                              "replica": f"replicas x{world} (no data-path collective)"}[shard]),
             "batch_total": job_batch,
             "summary_dtype": args.summary_dtype,
@@ -581,6 +586,8 @@ def main():
     ap.add_argument("--page-size", type=int, default=None, help="override the config's page size (16/32)")
     ap.add_argument("--kv-gib", type=float, default=None,
                     help="KV pool budget per GPU (default: all free HBM minus headroom)")
+    ap.add_argument("--transport", default="p2p", choices=["p2p", "nccl"],
+                    help="head shard score exchange: peer-memory stores fused into the scan, or NCCL all-gather")
     ap.add_argument("--shard", default="auto", choices=["auto", "batch", "head", "replica"],
                     help="multi-GPU partitioning (auto: cfg4 batch, cfg5 kv-head, else replicas)")
     args = ap.parse_args()

@@ -32,7 +32,7 @@
 extern "C" {
 #endif
 
-#define CHESS_ABI_VERSION 3
+#define CHESS_ABI_VERSION 4
 
 /* Status codes.  Python shim maps them to the pagesel exception classes
  * (pagesel/errors.py:4-21 and the ValueError/IndexError sites listed). */
@@ -263,6 +263,44 @@ int chess_select_partial(const ChessState* st, const ChessSelectCfg* cfg, int32_
                          double* partial, int64_t ld_partial, void* stream);
 int chess_select_combine(const ChessState* st, const ChessSelectCfg* cfg, int32_t level,
                          const double* gathered, int32_t world, int64_t ld_partial, void* stream);
+
+/* The same exchange over peer memory instead of a library all-gather: the
+ * partial scan's tail stores its rows straight into every rank's receive
+ * buffer (NVLink stores through peer-mapped pointers) and release-stores a
+ * per-(slot, source) flag; pull waits for the flags (acquire, system scope),
+ * adds the rows in rank order and finishes the level like
+ * chess_select_combine.  No host round trip and no collective launch per
+ * level; CUDA-graph capturable (generations live on the device).
+ * Per level, on every rank:
+ *   recv[p]  : DEVICE array of world pointers; recv[p] is rank p's receive
+ *              buffer, f64 [2][world][batch][ld] (double-buffered by gen & 1)
+ *   flags[p] : DEVICE array of world pointers; rank p's u32 [batch][world]
+ *   my_recv, my_flags : this rank's own entries (recv[rank], flags[rank])
+ *   gen      : this rank's u32 [batch] exchanges completed per slot
+ *   err      : this rank's i32 [1], set to 1 by a pull wait > 10 s
+ * recv/flags/gen/err zeroed before the first exchange; every rank calls
+ * push(level) then pull(level) in the same level order.  chess_p2p_* give
+ * IPC-shareable device memory for the buffers (cudaMalloc + IPC handles). */
+typedef struct ChessPeerExchange {
+  int32_t world, rank;
+  int64_t ld;
+  double* const* recv;
+  uint32_t* const* flags;
+  double* my_recv;
+  uint32_t* my_flags;
+  uint32_t* gen;
+  int32_t* err;
+} ChessPeerExchange;
+int chess_select_push(const ChessState* st, const ChessSelectCfg* cfg, int32_t level,
+                      const ChessPeerExchange* px, void* stream);
+int chess_select_pull(const ChessState* st, const ChessSelectCfg* cfg, int32_t level,
+                      const ChessPeerExchange* px, void* stream);
+#define CHESS_IPC_HANDLE_BYTES 64
+int chess_p2p_alloc(int64_t bytes, void** ptr);           /* zeroed device memory */
+int chess_p2p_free(void* ptr);
+int chess_p2p_export(void* ptr, uint8_t* handle);         /* handle: CHESS_IPC_HANDLE_BYTES */
+int chess_p2p_open(const uint8_t* handle, void** ptr);    /* peer's allocation in this process */
+int chess_p2p_close(void* ptr);
 
 /* K3 epilogue alone: rebuild working set + block table from the cached
  * semantic set for all slots (selection.py:126-140). */

@@ -21,7 +21,7 @@ from .errors import (
 )
 
 LIB_PATH = Path(__file__).resolve().parent / "libchess_b200.so"
-ABI_VERSION = 3
+ABI_VERSION = 4
 
 # enum ChessStatus
 OK, ERR_CONFIG, ERR_OUT_OF_PAGES, ERR_EMPTY_CONTEXT, ERR_SHAPE, ERR_INDEX, ERR_ORDER, ERR_VALUE, ERR_CUDA, ERR_UNSUPPORTED = range(10)
@@ -83,6 +83,20 @@ class ChessSelectCfg(C.Structure):
     ]
 
 
+class ChessPeerExchange(C.Structure):
+    _fields_ = [
+        ("world", C.c_int32),
+        ("rank", C.c_int32),
+        ("ld", C.c_int64),
+        ("recv", C.c_void_p),
+        ("flags", C.c_void_p),
+        ("my_recv", C.c_void_p),
+        ("my_flags", C.c_void_p),
+        ("gen", C.c_void_p),
+        ("err", C.c_void_p),
+    ]
+
+
 class ChessTriggerCfg(C.Structure):
     _fields_ = [
         ("policy", C.c_int32),
@@ -120,6 +134,15 @@ SIGNATURES = {
     "chess_pool_release": (C.c_int, [C.POINTER(ChessState), _P, _P]),
     "chess_select_partial": (C.c_int, [C.POINTER(ChessState), C.POINTER(ChessSelectCfg), _I32, _P, _I64, _P]),
     "chess_select_combine": (C.c_int, [C.POINTER(ChessState), C.POINTER(ChessSelectCfg), _I32, _P, _I32, _I64, _P]),
+    "chess_select_push": (C.c_int, [C.POINTER(ChessState), C.POINTER(ChessSelectCfg), _I32,
+                                    C.POINTER(ChessPeerExchange), _P]),
+    "chess_select_pull": (C.c_int, [C.POINTER(ChessState), C.POINTER(ChessSelectCfg), _I32,
+                                    C.POINTER(ChessPeerExchange), _P]),
+    "chess_p2p_alloc": (C.c_int, [_I64, C.POINTER(C.c_void_p)]),
+    "chess_p2p_free": (C.c_int, [_P]),
+    "chess_p2p_export": (C.c_int, [_P, C.c_char_p]),
+    "chess_p2p_open": (C.c_int, [C.c_char_p, C.POINTER(C.c_void_p)]),
+    "chess_p2p_close": (C.c_int, [_P]),
     "chess_build_working_set": (C.c_int, [C.POINTER(ChessState), _P]),
     "chess_flush_working_sets": (C.c_int, [C.POINTER(ChessState), _P]),
     "chess_sparse_decode": (C.c_int, [C.POINTER(ChessState), _I32, _P, _I64, _P, _I64, _P, _F, _P]),

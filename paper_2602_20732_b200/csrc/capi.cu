@@ -5,6 +5,7 @@
 // check happens before launch, no entry point synchronises its stream.
 #include <cstdarg>
 #include <cstdlib>
+#include <cstring>
 #include <mutex>
 
 #include "common.cuh"
@@ -27,6 +28,8 @@ int launch_pool_init(const ChessState&, const int32_t*, int, cudaStream_t);
 int launch_pool_reserve(const ChessState&, const int32_t*, cudaStream_t);
 int launch_pool_release(const ChessState&, const uint8_t*, cudaStream_t);
 int launch_select_partial(const ChessState&, const Workspace&, const SelParams&, int, cudaStream_t);
+int launch_select_pull(const ChessState&, const Workspace&, const SelParams&, int, const double*,
+                       const uint32_t*, uint32_t*, int32_t*, cudaStream_t);
 int launch_select_combine(const ChessState&, const Workspace&, const SelParams&, int,
                           const double*, int, cudaStream_t);
 int launch_build_ws_all(const ChessState&, cudaStream_t);
@@ -343,6 +346,75 @@ int chess_select_combine(const ChessState* st, const ChessSelectCfg* cfg, int32_
   if (!gathered || world < 1) return fail(CHESS_ERR_SHAPE, "select_combine: bad gathered buffer / world");
   prm.xld = ld_partial;
   return launch_select_combine(*st, ws, prm, level, gathered, world, (cudaStream_t)stream);
+}
+
+static int peer_params(const ChessState* st, const ChessSelectCfg* cfg, int32_t level,
+                       const ChessPeerExchange* px, SelParams* prm) {
+  int rc;
+  if ((rc = select_params(cfg, prm))) return rc;
+  if (!px) return fail(CHESS_ERR_CONFIG, "null peer exchange");
+  if ((rc = check_level(st, cfg, level, px->ld))) return rc;
+  if (px->world < 1 || px->rank < 0 || px->rank >= px->world)
+    return fail(CHESS_ERR_CONFIG, "peer exchange rank %d / world %d invalid", px->rank, px->world);
+  if (!px->recv || !px->flags || !px->gen || !px->err)
+    return fail(CHESS_ERR_CONFIG, "peer exchange: null recv/flags/gen/err");
+  prm->xpeer = px->recv;
+  prm->xflag = px->flags;
+  prm->xgen = px->gen;
+  prm->xrank = px->rank;
+  prm->xworld = px->world;
+  prm->xld = px->ld;
+  return CHESS_OK;
+}
+
+int chess_select_push(const ChessState* st, const ChessSelectCfg* cfg, int32_t level,
+                      const ChessPeerExchange* px, void* stream) {
+  Workspace ws;
+  int rc = state_ws(st, &ws);
+  if (rc) return rc;
+  SelParams prm;
+  if ((rc = peer_params(st, cfg, level, px, &prm))) return rc;
+  return launch_select_partial(*st, ws, prm, level, (cudaStream_t)stream);
+}
+
+int chess_select_pull(const ChessState* st, const ChessSelectCfg* cfg, int32_t level,
+                      const ChessPeerExchange* px, void* stream) {
+  Workspace ws;
+  int rc = state_ws(st, &ws);
+  if (rc) return rc;
+  SelParams prm;
+  if ((rc = peer_params(st, cfg, level, px, &prm))) return rc;
+  if (!px->my_recv || !px->my_flags) return fail(CHESS_ERR_CONFIG, "select_pull: null my_recv/my_flags");
+  return launch_select_pull(*st, ws, prm, level, px->my_recv, px->my_flags, px->gen, px->err, (cudaStream_t)stream);
+}
+
+int chess_p2p_alloc(int64_t bytes, void** ptr) {
+  if (!ptr || bytes <= 0) return fail(CHESS_ERR_CONFIG, "p2p_alloc: bad arguments");
+  if (cudaMalloc(ptr, (size_t)bytes) != cudaSuccess) return fail(CHESS_ERR_CUDA, "p2p_alloc: cudaMalloc");
+  if (cudaMemset(*ptr, 0, (size_t)bytes) != cudaSuccess) return fail(CHESS_ERR_CUDA, "p2p_alloc: memset");
+  return CHESS_OK;
+}
+int chess_p2p_free(void* ptr) {
+  return cudaFree(ptr) == cudaSuccess ? CHESS_OK : fail(CHESS_ERR_CUDA, "p2p_free");
+}
+int chess_p2p_export(void* ptr, uint8_t* handle) {
+  static_assert(sizeof(cudaIpcMemHandle_t) == CHESS_IPC_HANDLE_BYTES, "ipc handle size");
+  cudaIpcMemHandle_t h;
+  if (!ptr || !handle || cudaIpcGetMemHandle(&h, ptr) != cudaSuccess)
+    return fail(CHESS_ERR_CUDA, "p2p_export: cudaIpcGetMemHandle");
+  memcpy(handle, &h, sizeof(h));
+  return CHESS_OK;
+}
+int chess_p2p_open(const uint8_t* handle, void** ptr) {
+  cudaIpcMemHandle_t h;
+  if (!handle || !ptr) return fail(CHESS_ERR_CONFIG, "p2p_open: null argument");
+  memcpy(&h, handle, sizeof(h));
+  if (cudaIpcOpenMemHandle(ptr, h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess)
+    return fail(CHESS_ERR_CUDA, "p2p_open: cudaIpcOpenMemHandle");
+  return CHESS_OK;
+}
+int chess_p2p_close(void* ptr) {
+  return cudaIpcCloseMemHandle(ptr) == cudaSuccess ? CHESS_OK : fail(CHESS_ERR_CUDA, "p2p_close");
 }
 
 static int pool_state(const ChessState* st) {

@@ -99,6 +99,14 @@ struct SelParams {
   // xout[slot * xld + candidate]; select_combine_kernel finishes the level.
   double* xout;
   int64_t xld;
+  // Peer-memory transport of the same exchange (chess_select_push): the tail
+  // stores the partial row straight into every peer's receive buffer
+  // xpeer[p][(gen&1)][xrank][slot][xld] over NVLink and release-stores
+  // xflag[p][slot * xworld + xrank] = gen + 1 (gen = xgen[slot]).
+  double* const* xpeer;
+  uint32_t* const* xflag;
+  const uint32_t* xgen;
+  int32_t xrank, xworld;
 };
 
 // ---------------------------------------------------------------------------
@@ -332,6 +340,15 @@ __device__ __forceinline__ int ld_acquire_gpu(const int* p) {
 }
 __device__ __forceinline__ void st_release_gpu(int* p, int v) {
   asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+// system scope (peer GPU memory over NVLink)
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.sys.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
 // explicit shared-window vector loads (a generic pointer into dynamic smem

@@ -182,13 +182,30 @@ __device__ void select_tail(const ChessState& st, const Workspace& ws, const Sel
       for (int q = 1; q < 16; ++q)
         if (q0 + q < ns) acc = __dadd_rn(acc, v[q]);
     }
-    if (prm.xout)
+    if (prm.xpeer) {
+      // peer-memory all-gather fused into the scan: this rank's partial row
+      // goes straight into every rank's receive slot (NVLink stores)
+      const int64_t off =
+          (((int64_t)(prm.xgen[s] & 1u) * prm.xworld + prm.xrank) * st.d.batch + s) * prm.xld + i;
+      for (int p = 0; p < prm.xworld; ++p) prm.xpeer[p][off] = acc;
+    } else if (prm.xout) {
       prm.xout[(int64_t)s * prm.xld + i] = acc;
-    else
+    } else {
       sc[i] = acc;
+    }
   }
   block_sync<kNT>();
   tail_trace(level, s, 2);
+  if (prm.xpeer) {
+    // every thread's stores precede thread 0's system-scope fence (bar.sync
+    // above); the flag then publishes the row to each receiver
+    if (threadIdx.x == 0) {
+      __threadfence_system();
+      const uint32_t g = prm.xgen[s] + 1u;
+      for (int p = 0; p < prm.xworld; ++p) st_release_sys(prm.xflag[p] + s * prm.xworld + prm.xrank, g);
+    }
+    return;
+  }
   if (prm.xout) return;  // head shard: exchange, then select_combine_kernel finishes the level
   select_tail_topk(st, ws, prm, s, level, n, sm);
 }
@@ -1118,6 +1135,50 @@ __global__ void __launch_bounds__(kNT) select_combine_kernel(ChessState st, Work
   select_tail_topk(st, ws, prm, s, level, n, sm);
 }
 
+// Receive side of the peer-memory transport (chess_select_pull): wait for
+// every rank's flag of this slot to reach gen + 1 (acquire, system scope),
+// add the rows of receive buffer (gen & 1) in rank order, advance gen, top-k.
+// Two buffers suffice: a rank writes generation g + 2 into the buffer of g
+// only after its pull of g + 1, which needs this rank's push of g + 1, which
+// stream order places after this pull of g.  A wait longer than 10 s sets
+// *err (the host raises) instead of hanging the device.
+__global__ void __launch_bounds__(kNT) select_pull_kernel(ChessState st, Workspace ws, SelParams prm,
+                                                          int level, const double* recv,
+                                                          const uint32_t* flags, uint32_t* gen,
+                                                          int32_t* err) {
+  __shared__ TailSmem sm;
+  const int s = blockIdx.x;
+  const int n = level_rows(st, ws, prm, s, level);
+  if (n == 0) return;
+  const int world = prm.xworld;
+  const uint32_t g = gen[s];
+  if (threadIdx.x < world) {
+    const uint32_t* f = flags + s * world + threadIdx.x;
+    const uint64_t t0 = global_ns();
+    uint32_t polls = 0;
+    // wrap-safe "flag >= g + 1"
+    while ((int32_t)(ld_acquire_sys(f) - (g + 1u)) < 0) {
+      if ((++polls & 255u) == 0 && global_ns() - t0 > 10000000000ull) {
+        atomicExch(err, 1);
+        break;
+      }
+    }
+  }
+  block_sync<kNT>();
+  const int64_t mr = max_rows(st.d);
+  const int64_t rstride = (int64_t)st.d.batch * prm.xld;
+  const double* b = recv + ((int64_t)(g & 1u) * world * st.d.batch + s) * prm.xld;
+  double* sc = ws.scores + (int64_t)s * mr;
+  for (int i = threadIdx.x; i < n; i += kNT) {
+    double acc = __ldcg(b + i);
+    for (int r = 1; r < world; ++r) acc = __dadd_rn(acc, __ldcg(b + r * rstride + i));
+    sc[i] = acc;
+  }
+  block_sync<kNT>();
+  if (threadIdx.x == 0) gen[s] = g + 1u;
+  select_tail_topk(st, ws, prm, s, level, n, sm);
+}
+
 // ---------------------------------------------------------------------------
 // generic function-level kernels
 // ---------------------------------------------------------------------------
@@ -1380,13 +1441,13 @@ int launch_select(const ChessState& st, const Workspace& ws, const SelParams& pr
   // measured slower than three per-level launches (tools/select_micro.py:
   // cfg3 378 vs 308 us, cfg2 45 vs 38 us) — kept for further work.
   static const int flow_env = getenv("CHESS_SELECT_FLOW") ? atoi(getenv("CHESS_SELECT_FLOW")) : 0;
-  if (flow_env && !prm.full_scan && !prm.xout && prm.mode == 0 && st.d.batch <= kFlowMaxBatch)
+  if (flow_env && !prm.full_scan && !prm.xout && !prm.xpeer && prm.mode == 0 && st.d.batch <= kFlowMaxBatch)
     return st.d.summary_dtype == 0 ? launch_flow<float>(st, ws, prm, stream)
            : st.d.summary_dtype == 2 ? launch_flow<__nv_bfloat16>(st, ws, prm, stream)
                                      : launch_flow<double>(st, ws, prm, stream);
   // short rows: the whole cascade of a slot in one CTA (CHESS_SELECT_SMALL=0 to A/B)
   static const int small_env = getenv("CHESS_SELECT_SMALL") ? atoi(getenv("CHESS_SELECT_SMALL")) : 1;
-  if (small_env && !prm.full_scan && !prm.xout && prm.mode == 0 &&
+  if (small_env && !prm.full_scan && !prm.xout && !prm.xpeer && prm.mode == 0 &&
       st.d.ld * summary_elem_bytes(st.d.summary_dtype) <= kSmallRowBytes) {
     if (st.d.summary_dtype == 0)
       select_small_kernel<float><<<st.d.batch, kNT, 0, stream>>>(st, ws, prm);
@@ -1419,6 +1480,13 @@ int launch_select_combine(const ChessState& st, const Workspace& ws, const SelPa
                           int level, const double* gathered, int world, cudaStream_t stream) {
   select_combine_kernel<<<st.d.batch, kNT, 0, stream>>>(st, ws, prm, level, gathered, world);
   return check_launch("select_combine");
+}
+
+int launch_select_pull(const ChessState& st, const Workspace& ws, const SelParams& prm, int level,
+                       const double* recv, const uint32_t* flags, uint32_t* gen, int32_t* err,
+                       cudaStream_t stream) {
+  select_pull_kernel<<<st.d.batch, kNT, 0, stream>>>(st, ws, prm, level, recv, flags, gen, err);
+  return check_launch("select_pull");
 }
 
 int launch_build_ws_all(const ChessState& st, cudaStream_t stream);

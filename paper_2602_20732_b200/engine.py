@@ -172,11 +172,7 @@ class ChessDecoder:
     def _select_levels(self, cfg, sp):
         x = self.exchange
         for lv in x.levels:
-            _lib.call("chess_select_partial", self.state.ref, C.byref(cfg), lv,
-                      _lib.ptr(x.partial[lv]), x.ld[lv], sp)
-            gathered = x.scores(lv)
-            _lib.call("chess_select_combine", self.state.ref, C.byref(cfg), lv,
-                      _lib.ptr(gathered), x.world, x.ld[lv], sp)
+            x.select_level(self.state, cfg, lv, sp)
 
     def initial_selection(self, stream=None):
         """Post-prefill selection (simulate.py:147-151); 'never' keeps every page."""

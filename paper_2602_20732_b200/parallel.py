@@ -122,6 +122,18 @@ class HeadShardExchange:
         # output as [world * rows, ...] (rank blocks concatenated on dim 0)
         dist.all_gather_into_tensor(out.view(-1, *inp.shape[1:]), inp, group=self.group)
 
+    def select_level(self, state, cfg, level, stream_ptr) -> None:
+        """One cascade level: partial scan -> all-gather -> rank-ordered combine."""
+        import ctypes as C
+
+        from . import _lib
+
+        _lib.call("chess_select_partial", state.ref, C.byref(cfg), level, _lib.ptr(self.partial[level]),
+                  self.ld[level], stream_ptr)
+        gathered = self.scores(level)
+        _lib.call("chess_select_combine", state.ref, C.byref(cfg), level, _lib.ptr(gathered), self.world,
+                  self.ld[level], stream_ptr)
+
     def scores(self, level: int) -> torch.Tensor:
         self._allgather(self.gathered[level], self.partial[level])
         return self.gathered[level]
@@ -130,6 +142,130 @@ class HeadShardExchange:
         """gather_buf [world, batch, H_q/n, d]; this rank's block is filled."""
         self._allgather(gather_buf, gather_buf[self.rank])
         return gather_buf
+
+
+class PeerScoreExchange(HeadShardExchange):
+    """The score exchange of the KV-head shard over peer memory (NVLink).
+
+    Each level is two launches instead of partial -> NCCL all-gather ->
+    combine: `chess_select_push` is the partial scan whose tail stores the
+    rank's partial rows straight into every rank's receive buffer through
+    peer-mapped pointers and release-stores a per-(slot, source) flag;
+    `chess_select_pull` waits on its own flags, sums the rows in rank order
+    (bit-identical across ranks, as the NCCL path) and finishes the level.
+    The all-gather is thereby fused into the scan's epilogue: no collective
+    launch, no host involvement, graph capturable (generations on device).
+
+    Memory: one `chess_p2p_alloc` region per rank (cudaMalloc, so its IPC
+    handle maps the whole region), per level recv f64 [2][world][batch][ld]
+    then flags u32 [batch][world], 256-byte aligned; the same offsets on
+    every rank.
+    `connect(group)` shares the IPC handles over torch.distributed (any
+    backend) and opens the peers' regions; `connect_local(xs)` wires
+    in-process rank objects (single-GPU tests).  Outputs are still gathered
+    by the inherited all-gather.
+    """
+
+    def __init__(self, shard, batch, max_pages, pages_per_chunk, chunks_per_grid, device,
+                 group=None, full_scan=False, allgather=None):
+        import ctypes as C
+
+        from . import _lib
+
+        super().__init__(shard, batch, max_pages, pages_per_chunk, chunks_per_grid, device, group=group,
+                         full_scan=full_scan, allgather=allgather)
+        self.batch, self.device = batch, torch.device(device)
+        self.offsets, self.nbytes = self.layout(self.world, batch, self.ld)
+        base = C.c_void_p()
+        with torch.cuda.device(self.device):
+            _lib.call("chess_p2p_alloc", self.nbytes, C.byref(base))
+        self.base = base.value
+        self._opened = []
+        self.gen = {lv: torch.zeros(batch, dtype=torch.int32, device=self.device) for lv in self.levels}
+        self.err = torch.zeros(1, dtype=torch.int32, device=self.device)
+        self.px = None
+
+    @staticmethod
+    def layout(world: int, batch: int, ld: dict) -> tuple[dict, int]:
+        """{level: (recv offset, flags offset)} and the region size (bytes)."""
+        def up(x):
+            return (x + 255) // 256 * 256
+
+        off, out = 0, {}
+        for lv in sorted(ld):
+            recv = off
+            flags = up(recv + 2 * world * batch * ld[lv] * 8)
+            off = up(flags + batch * world * 4)
+            out[lv] = (recv, flags)
+        return out, off
+
+    def connect_local(self, exchanges) -> None:
+        self._wire([x.base for x in exchanges])
+
+    def connect(self, group=None) -> None:
+        import ctypes as C
+
+        from . import _lib
+
+        if self.world == 1:
+            self._wire([self.base])
+            return
+        h = C.create_string_buffer(64)
+        _lib.call("chess_p2p_export", C.c_void_p(self.base), h)
+        handles = [None] * self.world
+        dist.all_gather_object(handles, bytes(h.raw), group=group if group is not None else self.group)
+        bases = []
+        for r, hb in enumerate(handles):
+            if r == self.rank:
+                bases.append(self.base)
+                continue
+            p = C.c_void_p()
+            with torch.cuda.device(self.device):
+                _lib.call("chess_p2p_open", C.create_string_buffer(hb, 64), C.byref(p))
+            self._opened.append(p.value)
+            bases.append(p.value)
+        self._wire(bases)
+
+    def _wire(self, bases) -> None:
+        from . import _lib
+
+        if len(bases) != self.world:
+            raise ValueError(f"{len(bases)} peer regions for world {self.world}")
+        self.px, self._ptrs = {}, {}
+        for lv in self.levels:
+            ro, fo = self.offsets[lv]
+            recv = torch.tensor([b + ro for b in bases], dtype=torch.int64, device=self.device)
+            flags = torch.tensor([b + fo for b in bases], dtype=torch.int64, device=self.device)
+            self._ptrs[lv] = (recv, flags)
+            self.px[lv] = _lib.ChessPeerExchange(
+                self.world, self.rank, self.ld[lv], recv.data_ptr(), flags.data_ptr(),
+                self.base + ro, self.base + fo, self.gen[lv].data_ptr(), self.err.data_ptr())
+
+    def select_level(self, state, cfg, level, stream_ptr) -> None:
+        import ctypes as C
+
+        from . import _lib
+
+        if self.px is None:
+            raise RuntimeError("PeerScoreExchange not connected (connect / connect_local)")
+        px = C.byref(self.px[level])
+        _lib.call("chess_select_push", state.ref, C.byref(cfg), level, px, stream_ptr)
+        _lib.call("chess_select_pull", state.ref, C.byref(cfg), level, px, stream_ptr)
+
+    def check(self) -> None:
+        """Raise if a pull wait timed out (a peer never pushed)."""
+        if int(self.err.item()):
+            raise RuntimeError("peer score exchange: a pull wait timed out (ranks out of step?)")
+
+    def close(self) -> None:
+        from . import _lib
+
+        for p in self._opened:
+            _lib.call("chess_p2p_close", p)
+        self._opened = []
+        if self.base:
+            _lib.call("chess_p2p_free", self.base)
+            self.base = None
 
 
 def allgather_sum_scores(partial: torch.Tensor, group=None) -> torch.Tensor:

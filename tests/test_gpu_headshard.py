@@ -25,7 +25,7 @@ from oracle import pagesel_ref as ref
 from paper_2602_20732_b200 import _lib
 from paper_2602_20732_b200.config import SelectionConfig, preset_config
 from paper_2602_20732_b200.engine import ChessDecoder
-from paper_2602_20732_b200.parallel import HeadShard, HeadShardExchange
+from paper_2602_20732_b200.parallel import HeadShard, HeadShardExchange, PeerScoreExchange
 from paper_2602_20732_b200.state import DecodeState, Shape
 
 pytestmark = pytest.mark.gpu
@@ -140,8 +140,9 @@ class _ThreadAllGather:
         return allgather
 
 
+@pytest.mark.parametrize("transport", ["nccl", "p2p"])
 @pytest.mark.parametrize("world", [2, 4])
-def test_head_shard_decode_step_matches_unsharded(world):
+def test_head_shard_decode_step_matches_unsharded(world, transport):
     """Whole engine step: append -> L x (K4 + output gather) -> entropy ->
     seal -> level-by-level selection with the score exchange."""
     torch.manual_seed(world)
@@ -187,28 +188,42 @@ def test_head_shard_decode_step_matches_unsharded(world):
     group = _ThreadAllGather(world)
     results = [None] * world
     errors = []
+    # p2p: the score exchange over peer pointers (here: one device, in-process
+    # ranks on their own streams, so a pull really waits for another rank's push)
+    xs = [(PeerScoreExchange if transport == "p2p" else HeadShardExchange)(
+        HeadShard(r, world, L, H, Hq, d), batch, max_pages, 8, 8, "cuda", allgather=group.for_rank(r))
+        for r in range(world)]
+    if transport == "p2p":
+        for x in xs:
+            x.connect_local(xs)
+    streams = [torch.cuda.Stream() for _ in range(world)]
 
     def rank_main(r):
         try:
-            sh = HeadShard(r, world, L, H, Hq, d)
-            shape = Shape(**{**full_shape.__dict__, "kv_heads": hk, "q_heads": hq})
-            st = setup(shape, k_pool[:, :, r * hk:(r + 1) * hk].contiguous(),
-                       v_pool[:, :, r * hk:(r + 1) * hk].contiguous())
-            x = HeadShardExchange(sh, batch, max_pages, 8, 8, "cuda", allgather=group.for_rank(r))
-            dec = ChessDecoder(st, cfg, policy="every_step", exchange=x)
-            dec.build_index(n_now)
-            dec.initial_selection()
-            out = torch.zeros((3, L, world, batch, hq, d), device="cuda", dtype=torch.bfloat16)
-            for t in range(3):
-                kl = k_new[t][:, :, r * hk:(r + 1) * hk].reshape(batch, -1).contiguous()
-                vl = v_new[t][:, :, r * hk:(r + 1) * hk].reshape(batch, -1).contiguous()
-                ql = q[t][:, :, r * hq:(r + 1) * hq].contiguous()
-                dec.step(kl, vl, ql, logits[t], out[t])
-            torch.cuda.synchronize()
-            results[r] = (st, out)
+            with torch.cuda.stream(streams[r]):
+                rank_body(r)
         except Exception as e:  # pragma: no cover - surfaced below
             errors.append(e)
             group.barrier.abort()
+
+    def rank_body(r):
+        shape = Shape(**{**full_shape.__dict__, "kv_heads": hk, "q_heads": hq})
+        st = setup(shape, k_pool[:, :, r * hk:(r + 1) * hk].contiguous(),
+                   v_pool[:, :, r * hk:(r + 1) * hk].contiguous())
+        x = xs[r]
+        dec = ChessDecoder(st, cfg, policy="every_step", exchange=x)
+        dec.build_index(n_now)
+        dec.initial_selection()
+        out = torch.zeros((3, L, world, batch, hq, d), device="cuda", dtype=torch.bfloat16)
+        for t in range(3):
+            kl = k_new[t][:, :, r * hk:(r + 1) * hk].reshape(batch, -1).contiguous()
+            vl = v_new[t][:, :, r * hk:(r + 1) * hk].reshape(batch, -1).contiguous()
+            ql = q[t][:, :, r * hq:(r + 1) * hq].contiguous()
+            dec.step(kl, vl, ql, logits[t], out[t])
+        torch.cuda.synchronize()
+        if transport == "p2p":
+            x.check()
+        results[r] = (st, out)
 
     threads = [threading.Thread(target=rank_main, args=(r,)) for r in range(world)]
     for th in threads:
@@ -217,6 +232,9 @@ def test_head_shard_decode_step_matches_unsharded(world):
         th.join()
     if errors:
         raise errors[0]
+    for x in xs:
+        if transport == "p2p":
+            x.close()
     for r, (st, out) in enumerate(results):
         for s in range(batch):
             for name in ("semantic", "ws_logical", "block_table"):
@@ -228,3 +246,97 @@ def test_head_shard_decode_step_matches_unsharded(world):
         # merge order (not the math) differs: bf16-rounding tolerance
         err = (g.float() - out_full.float()).abs()
         assert torch.all(err <= 2.0**-7 * (out_full.float().abs() + 0.125)), (r, err.max())
+
+
+@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("full_scan", [False, True])
+def test_peer_exchange_selection(world, full_scan):
+    """chess_select_push / chess_select_pull: the all-gather fused into the
+    partial scan's tail over peer pointers.  In-process ranks on their own
+    streams, issued rank after rank, so every pull really waits for the other
+    ranks' pushes; repeated exchanges cycle both receive buffers; the last
+    rounds replay per-rank CUDA graphs.  Bars: the oracle's selection on every
+    rank, bit-identical across ranks, no wait timed out."""
+    from helpers import load_vectors, read_selection, set_tables
+
+    rng = np.random.default_rng(11 + world)
+    L, H, d, batch, max_pages = 2, 8, 16, 3, 500
+    D = L * H * d
+    cfg = SelectionConfig(pages_per_chunk=4, chunks_per_grid=5, rho_grid=0.5, rho_chunk=0.2, rho_page=0.1,
+                          window_pages=4, sink_pages=1)
+    states, xs, shards = [], [], []
+    for r in range(world):
+        sh = HeadShard(r, world, L, H, H, d)
+        shape = Shape(batch=batch, layers=L, kv_heads=H // world, q_heads=H // world, head_dim=d,
+                      page_size=cfg.page_size, pages_per_chunk=cfg.pages_per_chunk,
+                      chunks_per_grid=cfg.chunks_per_grid, max_pages=max_pages,
+                      window_pages=cfg.window_pages, max_ws=max_pages, n_phys=1)
+        states.append(DecodeState(shape))
+        shards.append(sh)
+        xs.append(PeerScoreExchange(sh, batch, max_pages, cfg.pages_per_chunk, cfg.chunks_per_grid, "cuda",
+                                    full_scan=full_scan))
+    for x in xs:
+        x.connect_local(xs)
+    expect = []
+    for slot in range(batch):
+        n = int(rng.integers(1, 450))
+        rows = rng.standard_normal((n, D))
+        for st, sh in zip(states, shards):
+            load_vectors(st, slot, rows[:, sh.flat_columns().numpy()])
+            set_tables(st, slot, n + 1, cfg.sink_pages)
+        h = ref.Hierarchy.from_rows(rows, cfg.pages_per_chunk, cfg.chunks_per_grid)
+        a, _ = ref.anchor(h.page_vectors, cfg.window_pages)
+        s = [m @ a for m in (h.grid_vectors, h.chunk_vectors, h.page_vectors)]
+        p2c, c2g = h.parent_maps()
+        sel, _ = ref.prune(s[0], s[1], s[2], p2c, c2g, cfg.ratios)
+        expect.append((sel, ref.working_set(sel, n + 1, cfg.window_pages, cfg.sink_pages)[0]))
+    torch.cuda.synchronize()
+    sc = _lib.ChessSelectCfg(cfg.rho_grid, cfg.rho_chunk, cfg.rho_page, int(full_scan), 1)
+    streams = [torch.cuda.Stream() for _ in range(world)]
+
+    def run_cascade(r):
+        for lv in _levels(full_scan):
+            xs[r].select_level(states[r], sc, lv, streams[r].cuda_stream)
+
+    def verify():
+        torch.cuda.synchronize()
+        for x in xs:
+            x.check()
+        for slot, (sel, pages) in enumerate(expect):
+            got0 = read_selection(states[0], slot)
+            np.testing.assert_array_equal(got0[0], sel)
+            np.testing.assert_array_equal(got0[1], pages)
+            for st in states[1:]:
+                for u, v in zip(got0, read_selection(st, slot)):
+                    np.testing.assert_array_equal(u, v)
+
+    rounds = 3
+    for _ in range(rounds):
+        for st in states:
+            st.ws_len.zero_()
+            st.n_semantic.zero_()
+        torch.cuda.synchronize()
+        for r in range(world):
+            run_cascade(r)
+        verify()
+    graphs = []
+    for r in range(world):
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(streams[r]):
+            with torch.cuda.graph(g, stream=streams[r]):
+                run_cascade(r)
+        graphs.append(g)
+    torch.cuda.synchronize()
+    for _ in range(2):
+        for st in states:
+            st.ws_len.zero_()
+            st.n_semantic.zero_()
+        torch.cuda.synchronize()
+        for r in range(world):
+            with torch.cuda.stream(streams[r]):
+                graphs[r].replay()
+        verify()
+    for x in xs:
+        for lv in x.levels:
+            assert torch.all(x.gen[lv] == rounds + 2), (lv, x.gen[lv])
+        x.close()

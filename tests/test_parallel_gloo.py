@@ -113,3 +113,23 @@ def test_shard_validation():
     with pytest.raises(ValueError):
         HeadShard(0, 3, 1, 8, 8, 4)
     assert list(BatchShard(3, 4, 128).slots) == list(range(96, 128))
+
+
+def test_peer_exchange_layout():
+    """Receive buffers / flags of the peer-memory score exchange: the same
+    offsets on every rank (each rank maps its peers' regions at these),
+    256-byte aligned blocks, no overlap."""
+    from paper_2602_20732_b200.parallel import PeerScoreExchange
+
+    for world, batch in ((1, 1), (2, 3), (8, 64)):
+        ld = {0: 7, 1: 33, 2: 250}
+        offs, total = PeerScoreExchange.layout(world, batch, ld)
+        spans = []
+        for lv, (ro, fo) in offs.items():
+            assert ro % 256 == 0 and fo % 256 == 0
+            spans.append((ro, ro + 2 * world * batch * ld[lv] * 8))
+            spans.append((fo, fo + batch * world * 4))
+        spans.sort()
+        for (a0, a1), (b0, b1) in zip(spans, spans[1:]):
+            assert a1 <= b0
+        assert spans[-1][1] <= total
