@@ -97,6 +97,18 @@ class ChessPeerExchange(C.Structure):
     ]
 
 
+class ChessPeerOutputs(C.Structure):
+    _fields_ = [
+        ("world", C.c_int32),
+        ("rank", C.c_int32),
+        ("regions", C.POINTER(C.c_void_p)),
+        ("flags", C.c_void_p),
+        ("my_flags", C.c_void_p),
+        ("gen", C.c_void_p),
+        ("err", C.c_void_p),
+    ]
+
+
 class ChessTriggerCfg(C.Structure):
     _fields_ = [
         ("policy", C.c_int32),
@@ -138,6 +150,9 @@ SIGNATURES = {
                                     C.POINTER(ChessPeerExchange), _P]),
     "chess_select_pull": (C.c_int, [C.POINTER(ChessState), C.POINTER(ChessSelectCfg), _I32,
                                     C.POINTER(ChessPeerExchange), _P]),
+    "chess_sparse_decode_gather": (C.c_int, [C.POINTER(ChessState), _I32, _P, _I64, _P, _F,
+                                             C.POINTER(ChessPeerOutputs), _P]),
+    "chess_gather_finish": (C.c_int, [C.POINTER(ChessState), C.POINTER(ChessPeerOutputs), _P, _P]),
     "chess_p2p_alloc": (C.c_int, [_I64, C.POINTER(C.c_void_p)]),
     "chess_p2p_free": (C.c_int, [_P]),
     "chess_p2p_export": (C.c_int, [_P, C.c_char_p]),

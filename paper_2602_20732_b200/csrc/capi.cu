@@ -44,7 +44,9 @@ int launch_working_set(const int32_t*, int, int, int, int, const int32_t*, int32
 int launch_gather_pages(const int32_t*, int, const int64_t*, int, int32_t*, int32_t*,
                         cudaStream_t);
 int launch_sparse_decode(const ChessState&, const Workspace&, int, const void*, int64_t, void*,
-                         int64_t, float*, float, cudaStream_t);
+                         int64_t, float*, float, cudaStream_t, const PeerOut* = nullptr);
+int launch_gather_finish(uint32_t* const*, uint32_t*, int, int, uint32_t*, int32_t*, const void*, int64_t,
+                         void*, cudaStream_t);
 int launch_entropy_trigger(const ChessState&, const Workspace&, const float*, int64_t, int64_t,
                            const ChessTriggerCfg&, double*, cudaStream_t);
 int launch_entropy_logits(const Workspace&, const float*, int64_t, int64_t, int64_t, double*,
@@ -471,6 +473,54 @@ int chess_sparse_decode(const ChessState* st, int32_t layer, const void* q, int6
   if (q_stride < row || out_stride < row) return fail(CHESS_ERR_SHAPE, "sparse_decode: stride < q_heads*head_dim");
   return launch_sparse_decode(*st, ws, layer, q, q_stride, out, out_stride, lse, softmax_scale,
                               (cudaStream_t)stream);
+}
+
+static int check_peer_outputs(const ChessState* st, const ChessPeerOutputs* po) {
+  if (!st || !po) return fail(CHESS_ERR_CONFIG, "null state / peer outputs");
+  if (po->world < 1 || po->world > kMaxPeers || po->rank < 0 || po->rank >= po->world)
+    return fail(CHESS_ERR_CONFIG, "peer outputs: rank %d / world %d invalid (world <= %d)", po->rank, po->world,
+                kMaxPeers);
+  if (!po->regions || !po->flags || !po->my_flags || !po->gen || !po->err)
+    return fail(CHESS_ERR_CONFIG, "peer outputs: null regions/flags/my_flags/gen/err");
+  for (int p = 0; p < po->world; ++p)
+    if (!po->regions[p] || (reinterpret_cast<uintptr_t>(po->regions[p]) & 15))
+      return fail(CHESS_ERR_CONFIG, "peer outputs: region %d null or not 16-byte aligned", p);
+  return CHESS_OK;
+}
+
+// elements of one (layer, rank) block and of one half of a region
+static int64_t gather_block(const ChessDims& d) { return (int64_t)d.batch * d.q_heads * d.head_dim; }
+
+int chess_sparse_decode_gather(const ChessState* st, int32_t layer, const void* q, int64_t q_stride,
+                               float* lse, float softmax_scale, const ChessPeerOutputs* po, void* stream) {
+  Workspace ws;
+  int rc = state_ws(st, &ws);
+  if (rc) return rc;
+  if ((rc = check_peer_outputs(st, po))) return rc;
+  if (layer < 0 || layer >= st->d.layers) return fail(CHESS_ERR_INDEX, "layer %d out of range", layer);
+  const int64_t row = (int64_t)st->d.q_heads * st->d.head_dim;
+  if (!q || q_stride < row) return fail(CHESS_ERR_SHAPE, "sparse_decode_gather: null q / q_stride < q_heads*head_dim");
+  const int64_t blk = gather_block(st->d);
+  const int64_t off = ((int64_t)layer * po->world + po->rank) * blk;
+  PeerOut pe;
+  pe.n_peer = 0;
+  for (int p = 0; p < po->world; ++p)
+    if (p != po->rank) pe.peer_out[pe.n_peer++] = static_cast<__nv_bfloat16*>(po->regions[p]) + off;
+  pe.gen = po->gen;
+  pe.parity_stride = (int64_t)st->d.layers * po->world * blk;
+  void* own = static_cast<__nv_bfloat16*>(po->regions[po->rank]) + off;
+  return launch_sparse_decode(*st, ws, layer, q, q_stride, own, row, lse, softmax_scale, (cudaStream_t)stream,
+                              &pe);
+}
+
+int chess_gather_finish(const ChessState* st, const ChessPeerOutputs* po, void* out, void* stream) {
+  int rc;
+  if ((rc = check_peer_outputs(st, po))) return rc;
+  const int64_t half = (int64_t)st->d.layers * po->world * gather_block(st->d);
+  if (half % 8 || (reinterpret_cast<uintptr_t>(out) & 15))
+    return fail(CHESS_ERR_SHAPE, "gather_finish: output must be 16-byte aligned with a multiple of 8 elements");
+  return launch_gather_finish(po->flags, po->my_flags, po->world, po->rank, po->gen, po->err,
+                              po->regions[po->rank], half, out, (cudaStream_t)stream);
 }
 
 int chess_entropy_trigger(const ChessState* st, const float* logits, int64_t vocab, int64_t ld,

@@ -88,6 +88,15 @@ constexpr int kAttnWarpsMax = kAttnCtasMax * 8; // stream-K warps (partial slots
 
 size_t workspace_layout(const ChessDims& d, void* base, Workspace* ws);
 
+// head-shard output gather over peer memory (chess_sparse_decode_gather)
+constexpr int kMaxPeers = 8;
+struct PeerOut {
+  __nv_bfloat16* peer_out[kMaxPeers - 1];  // this rank's block in every other rank's region
+  int n_peer;
+  const uint32_t* gen;     // device step counter: rows go to half (gen & 1)
+  int64_t parity_stride;   // elements between the halves
+};
+
 struct SelParams {
   double rho[3];
   int32_t full_scan;

@@ -218,18 +218,27 @@ class ChessDecoder:
 
         Head shard (self.exchange set): D, H_q are this rank's; `out` is the
         per-layer gather buffer [L, world, b, H_q, d] — K4 writes the rank's
-        block and the exchange all-gathers it after every layer."""
+        block and the exchange all-gathers it after every layer, or (a
+        PeerScoreExchange with fused_outputs) K4 stores the block into every
+        rank's region and one chess_gather_finish per step fills `out`."""
         x = self.exchange
         self.append(k_new, v_new, stream)
         if self.concurrent_select and self.kind != "never":
             self._step_concurrent(q, logits, out, lse, entropy_out, stream)
             return
-        for layer in range(self.state.shape.layers):
-            o = out[:, layer] if x is None else out[layer, x.rank]
-            self.attend(layer, q[:, layer], o, None if lse is None else lse[layer], stream)
-            if x is not None:
-                with _on(stream):
-                    x.outputs(out[layer])
+        if x is not None and getattr(x, "fused_outputs", False):
+            # outputs gathered by K4's peer stores; one publish/wait/copy per step
+            sp = _lib.stream_ptr(stream)
+            for layer in range(self.state.shape.layers):
+                x.attend(self.state, layer, q[:, layer], None if lse is None else lse[layer], self.scale, sp)
+            x.finish_outputs(self.state, out, sp)
+        else:
+            for layer in range(self.state.shape.layers):
+                o = out[:, layer] if x is None else out[layer, x.rank]
+                self.attend(layer, q[:, layer], o, None if lse is None else lse[layer], stream)
+                if x is not None:
+                    with _on(stream):
+                        x.outputs(out[layer])
         self.entropy_trigger(logits, entropy_out, stream)
         self.seal(stream)
         if self.kind != "never":

@@ -162,12 +162,17 @@ class PeerScoreExchange(HeadShardExchange):
     every rank.
     `connect(group)` shares the IPC handles over torch.distributed (any
     backend) and opens the peers' regions; `connect_local(xs)` wires
-    in-process rank objects (single-GPU tests).  Outputs are still gathered
-    by the inherited all-gather.
+    in-process rank objects (single-GPU tests).
+
+    Outputs (fused_outputs=True): K4's epilogue stores each output row of the
+    rank's query heads into its block of every rank's output region
+    (chess_sparse_decode_gather), and one chess_gather_finish per step
+    publishes / waits / copies — no per-layer all-gather.  The region is
+    double-buffered by step parity (device counter), so graph replays work.
     """
 
     def __init__(self, shard, batch, max_pages, pages_per_chunk, chunks_per_grid, device,
-                 group=None, full_scan=False, allgather=None):
+                 group=None, full_scan=False, allgather=None, fused_outputs=True):
         import ctypes as C
 
         from . import _lib
@@ -175,7 +180,11 @@ class PeerScoreExchange(HeadShardExchange):
         super().__init__(shard, batch, max_pages, pages_per_chunk, chunks_per_grid, device, group=group,
                          full_scan=full_scan, allgather=allgather)
         self.batch, self.device = batch, torch.device(device)
-        self.offsets, self.nbytes = self.layout(self.world, batch, self.ld)
+        # per-layer output gather fused into K4's epilogue (chess_sparse_decode_gather)
+        self.fused_outputs = bool(fused_outputs)
+        self.out_elems = (shard.layers * self.world * batch * shard.local_q_heads * shard.head_dim
+                          if self.fused_outputs else 0)
+        self.offsets, self.nbytes = self.layout(self.world, batch, self.ld, self.out_elems)
         base = C.c_void_p()
         with torch.cuda.device(self.device):
             _lib.call("chess_p2p_alloc", self.nbytes, C.byref(base))
@@ -186,8 +195,10 @@ class PeerScoreExchange(HeadShardExchange):
         self.px = None
 
     @staticmethod
-    def layout(world: int, batch: int, ld: dict) -> tuple[dict, int]:
-        """{level: (recv offset, flags offset)} and the region size (bytes)."""
+    def layout(world: int, batch: int, ld: dict, out_elems: int = 0) -> tuple[dict, int]:
+        """{level: (recv offset, flags offset)} (+ {"out": (output region
+        offset, output flags offset)} when out_elems, the bf16 elements of one
+        half of the output region) and the region size (bytes)."""
         def up(x):
             return (x + 255) // 256 * 256
 
@@ -197,6 +208,11 @@ class PeerScoreExchange(HeadShardExchange):
             flags = up(recv + 2 * world * batch * ld[lv] * 8)
             off = up(flags + batch * world * 4)
             out[lv] = (recv, flags)
+        if out_elems:
+            region = off
+            flags = up(region + 2 * out_elems * 2)
+            off = up(flags + world * 4)
+            out["out"] = (region, flags)
         return out, off
 
     def connect_local(self, exchanges) -> None:
@@ -227,6 +243,8 @@ class PeerScoreExchange(HeadShardExchange):
         self._wire(bases)
 
     def _wire(self, bases) -> None:
+        import ctypes as C
+
         from . import _lib
 
         if len(bases) != self.world:
@@ -240,6 +258,34 @@ class PeerScoreExchange(HeadShardExchange):
             self.px[lv] = _lib.ChessPeerExchange(
                 self.world, self.rank, self.ld[lv], recv.data_ptr(), flags.data_ptr(),
                 self.base + ro, self.base + fo, self.gen[lv].data_ptr(), self.err.data_ptr())
+        if self.fused_outputs:
+            ro, fo = self.offsets["out"]
+            self._regions = (C.c_void_p * self.world)(*[b + ro for b in bases])
+            oflags = torch.tensor([b + fo for b in bases], dtype=torch.int64, device=self.device)
+            self.out_gen = torch.zeros(2, dtype=torch.int32, device=self.device)
+            self._ptrs["out"] = (oflags,)
+            self.po = _lib.ChessPeerOutputs(self.world, self.rank, self._regions, oflags.data_ptr(),
+                                            self.base + fo, self.out_gen.data_ptr(), self.err.data_ptr())
+
+    def attend(self, state, layer, q, lse, scale, stream_ptr) -> None:
+        """K4 for one layer with its output rows stored into every rank's region."""
+        import ctypes as C
+
+        from . import _lib
+
+        _lib.call("chess_sparse_decode_gather", state.ref, layer, _lib.ptr(q), q.stride(0), _lib.ptr(lse),
+                  scale, C.byref(self.po), stream_ptr)
+
+    def finish_outputs(self, state, out, stream_ptr) -> None:
+        """Publish this rank's step, wait for every rank's, copy the gathered
+        outputs [L, world, b, H_q/n, d] into `out` (contiguous)."""
+        import ctypes as C
+
+        from . import _lib
+
+        if out is not None and (not out.is_contiguous() or out.numel() != self.out_elems):
+            raise ValueError("finish_outputs: out must be a contiguous [L, world, b, H_q/n, d] buffer")
+        _lib.call("chess_gather_finish", state.ref, C.byref(self.po), _lib.ptr(out), stream_ptr)
 
     def select_level(self, state, cfg, level, stream_ptr) -> None:
         import ctypes as C

@@ -140,7 +140,7 @@ class _ThreadAllGather:
         return allgather
 
 
-@pytest.mark.parametrize("transport", ["nccl", "p2p"])
+@pytest.mark.parametrize("transport", ["nccl", "p2p", "p2p_scores"])
 @pytest.mark.parametrize("world", [2, 4])
 def test_head_shard_decode_step_matches_unsharded(world, transport):
     """Whole engine step: append -> L x (K4 + output gather) -> entropy ->
@@ -190,10 +190,16 @@ def test_head_shard_decode_step_matches_unsharded(world, transport):
     errors = []
     # p2p: the score exchange over peer pointers (here: one device, in-process
     # ranks on their own streams, so a pull really waits for another rank's push)
-    xs = [(PeerScoreExchange if transport == "p2p" else HeadShardExchange)(
-        HeadShard(r, world, L, H, Hq, d), batch, max_pages, 8, 8, "cuda", allgather=group.for_rank(r))
-        for r in range(world)]
-    if transport == "p2p":
+    # p2p also gathers the outputs from K4's epilogue; p2p_scores keeps the
+    # per-layer all-gather for them
+    p2p = transport != "nccl"
+    xs = [PeerScoreExchange(HeadShard(r, world, L, H, Hq, d), batch, max_pages, 8, 8, "cuda",
+                            allgather=group.for_rank(r), fused_outputs=transport == "p2p")
+          if p2p else
+          HeadShardExchange(HeadShard(r, world, L, H, Hq, d), batch, max_pages, 8, 8, "cuda",
+                            allgather=group.for_rank(r))
+          for r in range(world)]
+    if p2p:
         for x in xs:
             x.connect_local(xs)
     streams = [torch.cuda.Stream() for _ in range(world)]
@@ -221,7 +227,7 @@ def test_head_shard_decode_step_matches_unsharded(world, transport):
             ql = q[t][:, :, r * hq:(r + 1) * hq].contiguous()
             dec.step(kl, vl, ql, logits[t], out[t])
         torch.cuda.synchronize()
-        if transport == "p2p":
+        if p2p:
             x.check()
         results[r] = (st, out)
 
@@ -233,7 +239,7 @@ def test_head_shard_decode_step_matches_unsharded(world, transport):
     if errors:
         raise errors[0]
     for x in xs:
-        if transport == "p2p":
+        if p2p:
             x.close()
     for r, (st, out) in enumerate(results):
         for s in range(batch):

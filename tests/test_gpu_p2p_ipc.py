@@ -6,7 +6,6 @@ chess_select_push / chess_select_pull.  Same bars as the in-process test:
 the oracle's selection, identical on both ranks, no wait timed out.  On a
 multi-GPU node the same code maps the peer GPU's memory over NVLink."""
 
-import os
 
 import numpy as np
 import pytest
@@ -78,6 +77,112 @@ def _rank(rank, world, port, full_scan, q):
 
 @pytest.mark.parametrize("full_scan", [False, True])
 def test_peer_exchange_across_processes(full_scan):
+    _run(_rank, (full_scan,))
+
+
+def _rank_step(rank, world, port, q):
+    """Whole head-shard decode steps across processes: scores AND outputs over
+    IPC-mapped peer memory (no collective on the data path), eager then
+    replayed from a captured CUDA graph; checked against the unsharded decoder
+    run in the same process."""
+    import torch.distributed as dist
+
+    from paper_2602_20732_b200.config import preset_config
+    from paper_2602_20732_b200.engine import ChessDecoder
+    from paper_2602_20732_b200.parallel import HeadShard, PeerScoreExchange
+    from paper_2602_20732_b200.state import DecodeState, Shape
+
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)
+        torch.manual_seed(0)  # identical inputs in both processes
+        cfg = preset_config("aggressive", page_size=16)
+        L, H, Hq, d, B = 2, 4, 8, 64, 16
+        batch, n_ctx, max_pages, n_phys, T = 2, 80, 120, 260, 4
+        full_shape = Shape(batch=batch, layers=L, kv_heads=H, q_heads=Hq, head_dim=d, page_size=B,
+                           pages_per_chunk=8, chunks_per_grid=8, max_pages=max_pages, window_pages=4,
+                           max_ws=max_pages, n_phys=n_phys)
+        k_pool = (torch.randn((L, n_phys, H, B, d), device="cuda") / 8).to(torch.bfloat16)
+        v_pool = torch.randn((L, n_phys, H, B, d), device="cuda").to(torch.bfloat16)
+        k_new = (torch.randn((T, batch, L, H, d), device="cuda") / 8).to(torch.bfloat16)
+        v_new = torch.randn((T, batch, L, H, d), device="cuda").to(torch.bfloat16)
+        qs = torch.randn((T, batch, L, Hq, d), device="cuda").to(torch.bfloat16)
+        logits = torch.randn((T, batch, 3000), device="cuda")
+        table = (torch.stack([torch.arange(max_pages) + 130 * s for s in range(batch)]) % n_phys).to(torch.int32)
+        n_now = torch.full((batch,), n_ctx, dtype=torch.int32, device="cuda")
+
+        def setup(shape, kp, vp):
+            st = DecodeState(shape, kv_pool=(kp, vp))
+            st.reset()
+            st.page_table.copy_(table)
+            st.num_pages.fill_(n_ctx)
+            st.tail_fill.fill_(B)
+            st.token_count.fill_(n_ctx * B)
+            st.sink_count.fill_(1)
+            return st
+
+        full = setup(full_shape, k_pool.clone(), v_pool.clone())
+        dec_full = ChessDecoder(full, cfg, policy="every_step")
+        dec_full.build_index(n_now)
+        dec_full.initial_selection()
+        out_full = torch.zeros((T, batch, L, Hq, d), device="cuda", dtype=torch.bfloat16)
+        sel_full = []
+        for t in range(T):
+            dec_full.step(k_new[t].reshape(batch, -1), v_new[t].reshape(batch, -1), qs[t], logits[t], out_full[t])
+            sel_full.append((full.ws_len.clone(), full.block_table.clone()))
+
+        hk, hq = H // world, Hq // world
+        shape = Shape(**{**full_shape.__dict__, "kv_heads": hk, "q_heads": hq})
+        st = setup(shape, k_pool[:, :, rank * hk:(rank + 1) * hk].contiguous(),
+                   v_pool[:, :, rank * hk:(rank + 1) * hk].contiguous())
+        x = PeerScoreExchange(HeadShard(rank, world, L, H, Hq, d), batch, max_pages, 8, 8, "cuda:0")
+        x.connect()
+        dec = ChessDecoder(st, cfg, policy="every_step", exchange=x)
+        dec.build_index(n_now)
+        dec.initial_selection()
+        kl = k_new[:, :, :, rank * hk:(rank + 1) * hk].reshape(T, batch, -1).contiguous()
+        vl = v_new[:, :, :, rank * hk:(rank + 1) * hk].reshape(T, batch, -1).contiguous()
+        ql = qs[:, :, :, rank * hq:(rank + 1) * hq].contiguous()
+        out = torch.zeros((T, L, world, batch, hq, d), device="cuda", dtype=torch.bfloat16)
+        sels = []
+        dec.step(kl[0], vl[0], ql[0], logits[0], out[0])
+        sels.append((st.ws_len.clone(), st.block_table.clone()))
+        sk, sv, sq, slg = kl[0].clone(), vl[0].clone(), ql[0].clone(), logits[0].clone()
+        so = torch.zeros_like(out[0])
+        g = dec.capture(sk, sv, sq, slg, so)
+        for t in range(1, T):
+            sk.copy_(kl[t])
+            sv.copy_(vl[t])
+            sq.copy_(ql[t])
+            slg.copy_(logits[t])
+            g.replay()
+            out[t].copy_(so)
+            sels.append((st.ws_len.clone(), st.block_table.clone()))
+        torch.cuda.synchronize()
+        x.check()
+        for t in range(T):
+            assert torch.equal(sels[t][0], sel_full[t][0]), t
+            for s in range(batch):
+                n = int(sel_full[t][0][s])
+                assert torch.equal(sels[t][1][s, :n], sel_full[t][1][s, :n]), (t, s)
+        gathered = out.permute(0, 3, 1, 2, 4, 5).reshape(T, batch, L, Hq, d)
+        err = (gathered.float() - out_full.float()).abs()
+        assert torch.all(err <= 2.0**-7 * (out_full.float().abs() + 0.125)), float(err.max())
+        dist.barrier()
+        x.close()
+        q.put((rank, "ok"))
+    except Exception as e:
+        q.put((rank, repr(e)))
+        raise
+    finally:
+        dist.destroy_process_group()
+
+
+def test_peer_decode_step_across_processes():
+    _run(_rank_step, ())
+
+
+def _run(fn, extra):
     import socket
 
     with socket.socket() as sk:
@@ -86,11 +191,11 @@ def test_peer_exchange_across_processes(full_scan):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     world = 2
-    procs = [ctx.Process(target=_rank, args=(r, world, port, full_scan, q)) for r in range(world)]
+    procs = [ctx.Process(target=fn, args=(r, world, port, *extra, q)) for r in range(world)]
     for p in procs:
         p.start()
     for p in procs:
-        p.join(timeout=240)
+        p.join(timeout=300)
     res = {}
     while not q.empty():
         r, msg = q.get()
