@@ -296,21 +296,24 @@ int chess_select_push(const ChessState* st, const ChessSelectCfg* cfg, int32_t l
 int chess_select_pull(const ChessState* st, const ChessSelectCfg* cfg, int32_t level,
                       const ChessPeerExchange* px, void* stream);
 /* Per-layer output gather of the KV-head shard over peer memory: K4 stores
- * every output row of this rank's query heads into its block of EVERY rank's
- * output region (NVLink stores from the epilogue), so no all-gather follows
- * the layer; chess_gather_finish ends the step (publish + wait on per-rank
- * flags, system scope) and copies the gathered outputs out.
+ * every output row of this rank's query heads into its own `out` block and
+ * into its block of EVERY other rank's output region (NVLink stores from the
+ * epilogue), so no all-gather follows the layer; chess_gather_finish ends the
+ * step: a two-phase barrier on per-source flags (system scope: "written",
+ * then "copied out") around the copy of the peers' blocks of this rank's
+ * region into `out`, so no rank's next step overwrites a region before every
+ * rank copied it.
  *   regions[p] : HOST array of world pointers (this process's mappings);
- *                rank p's region, bf16 [2][layers][world][batch][q_heads*head_dim]
- *                (double-buffered by step parity), 16-byte aligned
+ *                rank p's region, bf16 [layers][world][batch][q_heads*head_dim],
+ *                16-byte aligned
  *   flags[p]   : DEVICE array of world pointers; rank p's u32 [world]
  *   my_flags   : this rank's flags (flags[rank])
  *   gen        : this rank's u32 [2] {steps finished, CTA counter}, zeroed
  *   err        : this rank's i32 [1], set by a wait > 10 s
- * Every rank runs chess_sparse_decode_gather for each layer and then
- * chess_gather_finish once per step; `out` (bf16 [layers][world][batch]
- * [q_heads*head_dim], or NULL) receives the step's gathered outputs.  Outputs
- * of step t stay in the region until every rank finished step t + 1. */
+ * Every rank runs chess_sparse_decode_gather for each layer (out = its
+ * [layer][rank] block of the step's output, out_stride = q_heads*head_dim)
+ * and then chess_gather_finish once per step with the whole output, bf16
+ * [layers][world][batch][q_heads*head_dim]. */
 typedef struct ChessPeerOutputs {
   int32_t world, rank;
   void* const* regions;
@@ -320,7 +323,8 @@ typedef struct ChessPeerOutputs {
   int32_t* err;
 } ChessPeerOutputs;
 int chess_sparse_decode_gather(const ChessState* st, int32_t layer, const void* q, int64_t q_stride,
-                               float* lse, float softmax_scale, const ChessPeerOutputs* po, void* stream);
+                               void* out, int64_t out_stride, float* lse, float softmax_scale,
+                               const ChessPeerOutputs* po, void* stream);
 int chess_gather_finish(const ChessState* st, const ChessPeerOutputs* po, void* out, void* stream);
 #define CHESS_IPC_HANDLE_BYTES 64
 int chess_p2p_alloc(int64_t bytes, void** ptr);           /* zeroed device memory */

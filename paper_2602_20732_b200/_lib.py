@@ -150,7 +150,7 @@ SIGNATURES = {
                                     C.POINTER(ChessPeerExchange), _P]),
     "chess_select_pull": (C.c_int, [C.POINTER(ChessState), C.POINTER(ChessSelectCfg), _I32,
                                     C.POINTER(ChessPeerExchange), _P]),
-    "chess_sparse_decode_gather": (C.c_int, [C.POINTER(ChessState), _I32, _P, _I64, _P, _F,
+    "chess_sparse_decode_gather": (C.c_int, [C.POINTER(ChessState), _I32, _P, _I64, _P, _I64, _P, _F,
                                              C.POINTER(ChessPeerOutputs), _P]),
     "chess_gather_finish": (C.c_int, [C.POINTER(ChessState), C.POINTER(ChessPeerOutputs), _P, _P]),
     "chess_p2p_alloc": (C.c_int, [_I64, C.POINTER(C.c_void_p)]),

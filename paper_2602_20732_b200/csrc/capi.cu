@@ -46,7 +46,7 @@ int launch_gather_pages(const int32_t*, int, const int64_t*, int, int32_t*, int3
 int launch_sparse_decode(const ChessState&, const Workspace&, int, const void*, int64_t, void*,
                          int64_t, float*, float, cudaStream_t, const PeerOut* = nullptr);
 int launch_gather_finish(uint32_t* const*, uint32_t*, int, int, uint32_t*, int32_t*, const void*, int64_t,
-                         void*, cudaStream_t);
+                         int64_t, void*, cudaStream_t);
 int launch_entropy_trigger(const ChessState&, const Workspace&, const float*, int64_t, int64_t,
                            const ChessTriggerCfg&, double*, cudaStream_t);
 int launch_entropy_logits(const Workspace&, const float*, int64_t, int64_t, int64_t, double*,
@@ -356,8 +356,9 @@ static int peer_params(const ChessState* st, const ChessSelectCfg* cfg, int32_t 
   if ((rc = select_params(cfg, prm))) return rc;
   if (!px) return fail(CHESS_ERR_CONFIG, "null peer exchange");
   if ((rc = check_level(st, cfg, level, px->ld))) return rc;
-  if (px->world < 1 || px->rank < 0 || px->rank >= px->world)
-    return fail(CHESS_ERR_CONFIG, "peer exchange rank %d / world %d invalid", px->rank, px->world);
+  if (px->world < 1 || px->world > kMaxPeers || px->rank < 0 || px->rank >= px->world)
+    return fail(CHESS_ERR_CONFIG, "peer exchange rank %d / world %d invalid (world <= %d)", px->rank, px->world,
+                kMaxPeers);
   if (!px->recv || !px->flags || !px->gen || !px->err)
     return fail(CHESS_ERR_CONFIG, "peer exchange: null recv/flags/gen/err");
   prm->xpeer = px->recv;
@@ -488,11 +489,12 @@ static int check_peer_outputs(const ChessState* st, const ChessPeerOutputs* po) 
   return CHESS_OK;
 }
 
-// elements of one (layer, rank) block and of one half of a region
+// elements of one (layer, rank) block of a region
 static int64_t gather_block(const ChessDims& d) { return (int64_t)d.batch * d.q_heads * d.head_dim; }
 
 int chess_sparse_decode_gather(const ChessState* st, int32_t layer, const void* q, int64_t q_stride,
-                               float* lse, float softmax_scale, const ChessPeerOutputs* po, void* stream) {
+                               void* out, int64_t out_stride, float* lse, float softmax_scale,
+                               const ChessPeerOutputs* po, void* stream) {
   Workspace ws;
   int rc = state_ws(st, &ws);
   if (rc) return rc;
@@ -500,27 +502,27 @@ int chess_sparse_decode_gather(const ChessState* st, int32_t layer, const void* 
   if (layer < 0 || layer >= st->d.layers) return fail(CHESS_ERR_INDEX, "layer %d out of range", layer);
   const int64_t row = (int64_t)st->d.q_heads * st->d.head_dim;
   if (!q || q_stride < row) return fail(CHESS_ERR_SHAPE, "sparse_decode_gather: null q / q_stride < q_heads*head_dim");
+  if (!out || out_stride != row)
+    return fail(CHESS_ERR_SHAPE, "sparse_decode_gather: out must be this rank's [batch][q_heads*head_dim] block "
+                "with out_stride == q_heads*head_dim");
   const int64_t blk = gather_block(st->d);
   const int64_t off = ((int64_t)layer * po->world + po->rank) * blk;
   PeerOut pe;
   pe.n_peer = 0;
   for (int p = 0; p < po->world; ++p)
     if (p != po->rank) pe.peer_out[pe.n_peer++] = static_cast<__nv_bfloat16*>(po->regions[p]) + off;
-  pe.gen = po->gen;
-  pe.parity_stride = (int64_t)st->d.layers * po->world * blk;
-  void* own = static_cast<__nv_bfloat16*>(po->regions[po->rank]) + off;
-  return launch_sparse_decode(*st, ws, layer, q, q_stride, own, row, lse, softmax_scale, (cudaStream_t)stream,
+  return launch_sparse_decode(*st, ws, layer, q, q_stride, out, row, lse, softmax_scale, (cudaStream_t)stream,
                               &pe);
 }
 
 int chess_gather_finish(const ChessState* st, const ChessPeerOutputs* po, void* out, void* stream) {
   int rc;
   if ((rc = check_peer_outputs(st, po))) return rc;
-  const int64_t half = (int64_t)st->d.layers * po->world * gather_block(st->d);
-  if (half % 8 || (reinterpret_cast<uintptr_t>(out) & 15))
+  const int64_t elems = (int64_t)st->d.layers * po->world * gather_block(st->d);
+  if (elems % 8 || (reinterpret_cast<uintptr_t>(out) & 15))
     return fail(CHESS_ERR_SHAPE, "gather_finish: output must be 16-byte aligned with a multiple of 8 elements");
   return launch_gather_finish(po->flags, po->my_flags, po->world, po->rank, po->gen, po->err,
-                              po->regions[po->rank], half, out, (cudaStream_t)stream);
+                              po->regions[po->rank], elems, gather_block(st->d), out, (cudaStream_t)stream);
 }
 
 int chess_entropy_trigger(const ChessState* st, const float* logits, int64_t vocab, int64_t ld,

@@ -93,8 +93,6 @@ constexpr int kMaxPeers = 8;
 struct PeerOut {
   __nv_bfloat16* peer_out[kMaxPeers - 1];  // this rank's block in every other rank's region
   int n_peer;
-  const uint32_t* gen;     // device step counter: rows go to half (gen & 1)
-  int64_t parity_stride;   // elements between the halves
 };
 
 struct SelParams {

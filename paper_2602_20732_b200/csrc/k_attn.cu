@@ -93,22 +93,17 @@ struct AttnArgs {
   int prefetch;  // pages past the first run prefetched into L2 before the PDL wait
   // Head-shard output gather over peer memory (chess_sparse_decode_gather):
   // every output row is also stored at the same offset from peer_out[p]
-  // (this rank's block in peer p's region, NVLink stores); with out_gen set
-  // the rows go to half (gen & 1) of the double-buffered regions.
+  // (this rank's block in peer p's region, NVLink stores).
   __nv_bfloat16* peer_out[kMaxPeers - 1];
   int n_peer;
-  const uint32_t* out_gen;
-  int64_t parity_stride;
   int mode;  // debug (CHESS_ATTN_MODE): 0 normal, 1 loads only (no math), 2 math only (no K/V loads), 5 exit at entry, 6 exit after the prologue, 7 force stream-K, 8 no PDL wait (timing only: ignores the previous kernel)
 };
 
 // one bf16 pair of an output row, to this rank's buffer and every peer's
 __device__ __forceinline__ void out_pair(const AttnArgs& a, __nv_bfloat16* orow, float x, float y) {
   const __nv_bfloat162 v = __floats2bfloat162_rn(x, y);
-  int64_t par = 0;
-  if (a.out_gen) par = (int64_t)(__ldcg(a.out_gen) & 1u) * a.parity_stride;
-  *reinterpret_cast<__nv_bfloat162*>(orow + par) = v;
-  const int64_t off = (orow - a.out) + par;
+  *reinterpret_cast<__nv_bfloat162*>(orow) = v;
+  const int64_t off = orow - a.out;
   for (int p = 0; p < a.n_peer; ++p) *reinterpret_cast<__nv_bfloat162*>(a.peer_out[p] + off) = v;
 }
 
@@ -1153,13 +1148,9 @@ int launch_sparse_decode(const ChessState& st, const Workspace& ws, int layer, c
   const ChessDims& d = st.d;
   AttnArgs a;
   a.n_peer = 0;
-  a.out_gen = nullptr;
-  a.parity_stride = 0;
   if (po) {
     a.n_peer = po->n_peer;
     for (int p = 0; p < po->n_peer; ++p) a.peer_out[p] = po->peer_out[p];
-    a.out_gen = po->gen;
-    a.parity_stride = po->parity_stride;
   }
   a.q = reinterpret_cast<const __nv_bfloat16*>(q);
   a.q_stride = q_stride;
@@ -1203,58 +1194,76 @@ int launch_sparse_decode(const ChessState& st, const Workspace& ws, int layer, c
               d.head_dim, gq, d.page_size);
 }
 
-// End of a step's peer-memory output gather: CTA 0 publishes "this rank's
-// blocks of step gen are written" to every rank (system-scope release after
-// a system fence; stream order puts it after this rank's K4 launches), every
-// CTA waits for all ranks' flags, copies half (gen & 1) of this rank's region
-// into `out`, and the last CTA advances gen.  Two halves: a rank writes step
-// g + 2 into g's half only after its finish of g + 1, which needs every
-// rank's publish of g + 1, which each rank issues after its finish (copy) of g.
-__global__ void __launch_bounds__(256) gather_finish_kernel(uint32_t* const* flags, uint32_t* my_flags,
-                                                            int world, int rank, uint32_t* gen,
-                                                            int32_t* err, const __nv_bfloat16* region,
-                                                            int64_t half, __nv_bfloat16* out) {
-  __shared__ uint32_t s_g;
-  if (threadIdx.x == 0) s_g = __ldcg(gen);
-  __syncthreads();
-  const uint32_t g = s_g;
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    __threadfence_system();
-    for (int p = 0; p < world; ++p) st_release_sys(flags[p] + rank, g + 1u);
-  }
+// End of a step's peer-memory output gather, a two-phase barrier on
+// per-source flags (system scope; value 2g+1 = "step g written", 2g+2 =
+// "step g copied out", g = steps finished on this rank): CTA 0 publishes
+// "written" (stream order puts it after this rank's K4 launches), every CTA
+// waits for all ranks' "written", copies the peers' blocks of this rank's
+// region into `out` (K4 stored the own blocks there directly); the
+// last CTA publishes "copied" and waits for every rank's "copied" before the
+// kernel ends, so no rank's next-step K4 can overwrite a region a peer has
+// not copied yet.  One region (no double buffer) and no device read in K4.
+__device__ __forceinline__ void wait_flags(const uint32_t* f, int world, uint32_t target, int32_t* err) {
   if (threadIdx.x < world) {
     const uint64_t t0 = global_ns();
     uint32_t polls = 0;
-    while ((int32_t)(ld_acquire_sys(my_flags + threadIdx.x) - (g + 1u)) < 0) {
+    while ((int32_t)(ld_acquire_sys(f + threadIdx.x) - target) < 0) {
       if ((++polls & 255u) == 0 && global_ns() - t0 > 10000000000ull) {
         atomicExch(err, 1);
         break;
       }
     }
   }
+}
+
+__global__ void __launch_bounds__(256) gather_finish_kernel(uint32_t* const* flags, uint32_t* my_flags,
+                                                            int world, int rank, uint32_t* gen,
+                                                            int32_t* err, const __nv_bfloat16* region,
+                                                            int64_t elems, int64_t blk, __nv_bfloat16* out) {
+  __shared__ uint32_t s_g;
+  __shared__ int s_last;
+  if (threadIdx.x == 0) s_g = __ldcg(gen);
   __syncthreads();
-  if (out) {
-    const uint4* src = reinterpret_cast<const uint4*>(region + (int64_t)(g & 1u) * half);
+  const uint32_t g = s_g;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    __threadfence_system();
+    for (int p = 0; p < world; ++p) st_release_sys(flags[p] + rank, 2u * g + 1u);
+  }
+  wait_flags(my_flags, world, 2u * g + 1u, err);
+  __syncthreads();
+  if (out && world > 1) {
+    // the peers' blocks only: K4 wrote this rank's own blocks into `out`
+    const uint4* src = reinterpret_cast<const uint4*>(region);
     uint4* dst = reinterpret_cast<uint4*>(out);
-    const int64_t n = half / 8;  // half % 8 == 0 (checked by the caller)
-    for (int64_t i = blockIdx.x * 256 + threadIdx.x; i < n; i += (int64_t)gridDim.x * 256) dst[i] = __ldcg(src + i);
+    const int64_t n = elems / 8, bv = blk / 8;  // elems, blk % 8 == 0 (checked by the caller)
+    for (int64_t i = blockIdx.x * 256 + threadIdx.x; i < n; i += (int64_t)gridDim.x * 256)
+      if ((int)((i / bv) % world) != rank) dst[i] = __ldcg(src + i);
   }
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence();
-    if (atomicAdd(gen + 1, 1u) == gridDim.x - 1) {
-      gen[1] = 0;
-      gen[0] = g + 1u;
-    }
+    s_last = atomicAdd(gen + 1, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!s_last) return;
+  if (threadIdx.x == 0) {
+    __threadfence();
+    for (int p = 0; p < world; ++p) st_release_sys(flags[p] + rank, 2u * g + 2u);
+  }
+  wait_flags(my_flags, world, 2u * g + 2u, err);
+  if (threadIdx.x == 0) {
+    gen[1] = 0;
+    gen[0] = g + 1u;
   }
 }
 
 int launch_gather_finish(uint32_t* const* flags, uint32_t* my_flags, int world, int rank, uint32_t* gen,
-                         int32_t* err, const void* region, int64_t half, void* out, cudaStream_t stream) {
-  const int64_t v = half / 8;
-  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(2 * num_sms(), (v + 255) / 256));
+                         int32_t* err, const void* region, int64_t elems, int64_t blk, void* out,
+                         cudaStream_t stream) {
+  const int64_t v = elems / 8;
+  const int grid = world == 1 ? 1 : (int)std::max<int64_t>(1, std::min<int64_t>(2 * num_sms(), (v + 255) / 256));
   gather_finish_kernel<<<grid, 256, 0, stream>>>(flags, my_flags, world, rank, gen, err,
-                                                 reinterpret_cast<const __nv_bfloat16*>(region), half,
+                                                 reinterpret_cast<const __nv_bfloat16*>(region), elems, blk,
                                                  reinterpret_cast<__nv_bfloat16*>(out));
   return check_launch("gather_finish");
 }

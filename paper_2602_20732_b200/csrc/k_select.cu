@@ -166,6 +166,14 @@ __device__ void select_tail(const ChessState& st, const Workspace& ws, const Sel
   double* sc = ws.scores + (int64_t)s * mr;
   const double* part = ws.part + (int64_t)s * mr * ns;
 
+  // peer-memory export: receive-slot base of this (gen, rank, slot) in every
+  // rank's buffer, loaded once (the stores below could alias the arrays)
+  double* xdst[kMaxPeers];
+  if (prm.xpeer) {
+    const int64_t off0 = (((int64_t)(__ldcg(prm.xgen + s) & 1u) * prm.xworld + prm.xrank) * st.d.batch + s) * prm.xld;
+#pragma unroll
+    for (int p = 0; p < kMaxPeers; ++p) xdst[p] = p < prm.xworld ? prm.xpeer[p] + off0 : nullptr;
+  }
   // fixed-order reduction over slices (deterministic); the slice partials of
   // a row are loaded together (one round trip) when ns <= 16
   for (int i = threadIdx.x; i < n; i += kNT) {
@@ -185,9 +193,9 @@ __device__ void select_tail(const ChessState& st, const Workspace& ws, const Sel
     if (prm.xpeer) {
       // peer-memory all-gather fused into the scan: this rank's partial row
       // goes straight into every rank's receive slot (NVLink stores)
-      const int64_t off =
-          (((int64_t)(prm.xgen[s] & 1u) * prm.xworld + prm.xrank) * st.d.batch + s) * prm.xld + i;
-      for (int p = 0; p < prm.xworld; ++p) prm.xpeer[p][off] = acc;
+#pragma unroll
+      for (int p = 0; p < kMaxPeers; ++p)
+        if (p < prm.xworld) xdst[p][i] = acc;
     } else if (prm.xout) {
       prm.xout[(int64_t)s * prm.xld + i] = acc;
     } else {
@@ -197,11 +205,10 @@ __device__ void select_tail(const ChessState& st, const Workspace& ws, const Sel
   block_sync<kNT>();
   tail_trace(level, s, 2);
   if (prm.xpeer) {
-    // every thread's stores precede thread 0's system-scope fence (bar.sync
-    // above); the flag then publishes the row to each receiver
+    // every thread's stores precede thread 0's system-scope release store
+    // (bar.sync above; release is cumulative), which publishes the row
     if (threadIdx.x == 0) {
-      __threadfence_system();
-      const uint32_t g = prm.xgen[s] + 1u;
+      const uint32_t g = __ldcg(prm.xgen + s) + 1u;
       for (int p = 0; p < prm.xworld; ++p) st_release_sys(prm.xflag[p] + s * prm.xworld + prm.xrank, g);
     }
     return;

@@ -230,7 +230,8 @@ class ChessDecoder:
             # outputs gathered by K4's peer stores; one publish/wait/copy per step
             sp = _lib.stream_ptr(stream)
             for layer in range(self.state.shape.layers):
-                x.attend(self.state, layer, q[:, layer], None if lse is None else lse[layer], self.scale, sp)
+                x.attend(self.state, layer, q[:, layer], out[layer, x.rank], None if lse is None else lse[layer],
+                         self.scale, sp)
             x.finish_outputs(self.state, out, sp)
         else:
             for layer in range(self.state.shape.layers):

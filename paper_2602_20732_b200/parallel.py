@@ -167,8 +167,8 @@ class PeerScoreExchange(HeadShardExchange):
     Outputs (fused_outputs=True): K4's epilogue stores each output row of the
     rank's query heads into its block of every rank's output region
     (chess_sparse_decode_gather), and one chess_gather_finish per step
-    publishes / waits / copies — no per-layer all-gather.  The region is
-    double-buffered by step parity (device counter), so graph replays work.
+    publishes / waits / copies (a two-phase flag barrier) — no per-layer
+    all-gather; step counters live on the device, so graph replays work.
     """
 
     def __init__(self, shard, batch, max_pages, pages_per_chunk, chunks_per_grid, device,
@@ -197,8 +197,8 @@ class PeerScoreExchange(HeadShardExchange):
     @staticmethod
     def layout(world: int, batch: int, ld: dict, out_elems: int = 0) -> tuple[dict, int]:
         """{level: (recv offset, flags offset)} (+ {"out": (output region
-        offset, output flags offset)} when out_elems, the bf16 elements of one
-        half of the output region) and the region size (bytes)."""
+        offset, output flags offset)} when out_elems, the bf16 elements of the
+        output region) and the region size (bytes)."""
         def up(x):
             return (x + 255) // 256 * 256
 
@@ -210,7 +210,7 @@ class PeerScoreExchange(HeadShardExchange):
             out[lv] = (recv, flags)
         if out_elems:
             region = off
-            flags = up(region + 2 * out_elems * 2)
+            flags = up(region + out_elems * 2)
             off = up(flags + world * 4)
             out["out"] = (region, flags)
         return out, off
@@ -267,18 +267,19 @@ class PeerScoreExchange(HeadShardExchange):
             self.po = _lib.ChessPeerOutputs(self.world, self.rank, self._regions, oflags.data_ptr(),
                                             self.base + fo, self.out_gen.data_ptr(), self.err.data_ptr())
 
-    def attend(self, state, layer, q, lse, scale, stream_ptr) -> None:
-        """K4 for one layer with its output rows stored into every rank's region."""
+    def attend(self, state, layer, q, out, lse, scale, stream_ptr) -> None:
+        """K4 for one layer: output rows into `out` (this rank's [layer, rank]
+        block, [b, H_q/n, d] contiguous) and into every peer's region."""
         import ctypes as C
 
         from . import _lib
 
-        _lib.call("chess_sparse_decode_gather", state.ref, layer, _lib.ptr(q), q.stride(0), _lib.ptr(lse),
-                  scale, C.byref(self.po), stream_ptr)
+        _lib.call("chess_sparse_decode_gather", state.ref, layer, _lib.ptr(q), q.stride(0), _lib.ptr(out),
+                  out.stride(0), _lib.ptr(lse), scale, C.byref(self.po), stream_ptr)
 
     def finish_outputs(self, state, out, stream_ptr) -> None:
-        """Publish this rank's step, wait for every rank's, copy the gathered
-        outputs [L, world, b, H_q/n, d] into `out` (contiguous)."""
+        """Publish this rank's step, wait for every rank's, copy the peers'
+        blocks into `out` [L, world, b, H_q/n, d] (contiguous)."""
         import ctypes as C
 
         from . import _lib
