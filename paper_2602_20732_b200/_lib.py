@@ -146,6 +146,7 @@ SIGNATURES = {
     "chess_pool_release": (C.c_int, [C.POINTER(ChessState), _P, _P]),
     "chess_select_partial": (C.c_int, [C.POINTER(ChessState), C.POINTER(ChessSelectCfg), _I32, _P, _I64, _P]),
     "chess_select_combine": (C.c_int, [C.POINTER(ChessState), C.POINTER(ChessSelectCfg), _I32, _P, _I32, _I64, _P]),
+    "chess_append_kv_layers": (C.c_int, [C.POINTER(ChessState), _I32, _I32, _P, _P, _I64, _P, _P]),
     "chess_select_push": (C.c_int, [C.POINTER(ChessState), C.POINTER(ChessSelectCfg), _I32,
                                     C.POINTER(ChessPeerExchange), _P]),
     "chess_select_pull": (C.c_int, [C.POINTER(ChessState), C.POINTER(ChessSelectCfg), _I32,

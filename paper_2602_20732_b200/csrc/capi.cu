@@ -14,7 +14,7 @@ namespace chess {
 
 int launch_reset(const ChessState&, const uint8_t*, cudaStream_t);
 int launch_append(const ChessState&, const Workspace&, const void*, const void*, int64_t,
-                  const uint8_t*, cudaStream_t);
+                  const uint8_t*, cudaStream_t, int64_t col0 = 0, int64_t ncols = -1, int post = 0);
 int launch_seal(const ChessState&, const Workspace&, cudaStream_t);
 int launch_build(const ChessState&, const int32_t*, cudaStream_t);
 int launch_from_vectors(const ChessState&, int, const double*, int, int64_t, const int32_t*,
@@ -224,6 +224,22 @@ int chess_append_kv(const ChessState* st, const void* k_rows, const void* v_rows
   if (rc) return rc;
   if (!k_rows || !v_rows || row_stride < st->d.dim) return fail(CHESS_ERR_SHAPE, "append: bad rows");
   return launch_append(*st, ws, k_rows, v_rows, row_stride, active, (cudaStream_t)stream);
+}
+
+int chess_append_kv_layers(const ChessState* st, int32_t layer_begin, int32_t layer_end, const void* k_rows,
+                           const void* v_rows, int64_t row_stride, const uint8_t* active, void* stream) {
+  Workspace ws;
+  int rc = state_ws(st, &ws);
+  if (rc) return rc;
+  const ChessDims& d = st->d;
+  if (layer_begin < 0 || layer_end > d.layers || layer_begin >= layer_end)
+    return fail(CHESS_ERR_INDEX, "append_kv_layers: layer range [%d, %d) invalid for %d layers", layer_begin,
+                layer_end, d.layers);
+  const int64_t per_layer = (int64_t)d.kv_heads * d.head_dim;
+  const int64_t ncols = (layer_end - layer_begin) * per_layer;
+  if (!k_rows || !v_rows || row_stride < ncols) return fail(CHESS_ERR_SHAPE, "append_kv_layers: bad rows");
+  return launch_append(*st, ws, k_rows, v_rows, row_stride, active, (cudaStream_t)stream,
+                       layer_begin * per_layer, ncols, layer_begin > 0 ? 1 : 0);
 }
 
 int chess_summary_seal(const ChessState* st, void* stream) {

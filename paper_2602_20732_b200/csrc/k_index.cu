@@ -177,10 +177,17 @@ __global__ void reset_kernel(ChessState st, const uint8_t* mask) {
 // append (kv_store.py:141-154) + running key sum + WS refresh on page open
 // grid: (ceil(D / (kNT*8)), batch)
 // ---------------------------------------------------------------------------
+// Columns [col0, col0 + ncols) of the flattened (layer, head, d) row; k_rows
+// / v_rows hold just those columns.  post == 0 (the token's first call, the
+// whole row for chess_append_kv): slot/row from the pre-append counters,
+// which the last CTA then publishes.  post == 1 (later layer ranges of the
+// same token, chess_append_kv_layers): the counters are already published,
+// so the token's row is tail_fill - 1 of the last page and nothing else moves.
 __global__ void __launch_bounds__(kNT) append_kernel(ChessState st, const __nv_bfloat16* k_rows,
                                                      const __nv_bfloat16* v_rows,
                                                      int64_t row_stride, const uint8_t* active,
-                                                     int32_t* done) {
+                                                     int32_t* done, int64_t col0, int64_t ncols,
+                                                     int post) {
   __shared__ int s_scratch[48];
   __shared__ int s_last;
   const int s = blockIdx.y;
@@ -189,23 +196,33 @@ __global__ void __launch_bounds__(kNT) append_kernel(ChessState st, const __nv_b
   const int B = d.page_size;
   const int np = st.num_pages[s];
   const int fill = st.tail_fill[s];
-  const bool open_new = (np == 0) || (fill >= B);
-  if (st.pool_free && open_new && st.pool_end[s] <= np) {
-    // device pool: the page this token opens was never reserved (pool empty)
-    if (blockIdx.x == 0 && threadIdx.x == 0) st.pool_oom[s] = 1;
-    return;
+  bool open_new;
+  int slot, row;
+  if (post) {
+    if (st.pool_free && st.pool_oom[s]) return;  // the token's first call was refused
+    open_new = fill == 1;
+    slot = np - 1;
+    row = fill - 1;
+  } else {
+    open_new = (np == 0) || (fill >= B);
+    if (st.pool_free && open_new && st.pool_end[s] <= np) {
+      // device pool: the page this token opens was never reserved (pool empty)
+      if (blockIdx.x == 0 && threadIdx.x == 0) st.pool_oom[s] = 1;
+      return;
+    }
+    slot = open_new ? np : np - 1;
+    row = open_new ? 0 : fill;
   }
-  const int slot = open_new ? np : np - 1;
-  const int row = open_new ? 0 : fill;
   const int64_t phys = st.page_table[(int64_t)s * d.max_pages + slot];
-  const __nv_bfloat16* kr = k_rows + (int64_t)s * row_stride;
-  const __nv_bfloat16* vr = v_rows + (int64_t)s * row_stride;
+  const __nv_bfloat16* kr = k_rows + (int64_t)s * row_stride - col0;
+  const __nv_bfloat16* vr = v_rows + (int64_t)s * row_stride - col0;
   double* ks = st.key_sum + (int64_t)s * d.ld;
   __nv_bfloat16* kp = reinterpret_cast<__nv_bfloat16*>(st.k_pool);
   __nv_bfloat16* vp = reinterpret_cast<__nv_bfloat16*>(st.v_pool);
+  const int64_t cend = col0 + ncols;
 
-  const int64_t j0 = ((int64_t)blockIdx.x * kNT + threadIdx.x) * 8;
-  if (j0 < d.dim) {
+  const int64_t j0 = col0 + ((int64_t)blockIdx.x * kNT + threadIdx.x) * 8;
+  if (j0 < cend) {
     if ((d.head_dim % 8) == 0 && (row_stride % 8) == 0) {
       const uint4 kv = *reinterpret_cast<const uint4*>(kr + j0);
       const uint4 vv = *reinterpret_cast<const uint4*>(vr + j0);
@@ -223,7 +240,7 @@ __global__ void __launch_bounds__(kNT) append_kernel(ChessState st, const __nv_b
     } else {
       for (int q = 0; q < 8; ++q) {
         const int64_t j = j0 + q;
-        if (j >= d.dim) break;
+        if (j >= cend) break;
         const int64_t off = pool_offset(d, j, phys, row);
         kp[off] = kr[j];
         vp[off] = vr[j];
@@ -232,6 +249,7 @@ __global__ void __launch_bounds__(kNT) append_kernel(ChessState st, const __nv_b
       }
     }
   }
+  if (post) return;
   // last CTA of this slot publishes the new counters (all CTAs read the
   // pre-state above before incrementing).
   __syncthreads();
@@ -589,12 +607,14 @@ int launch_pool_release(const ChessState& st, const uint8_t* mask, cudaStream_t 
 }
 
 int launch_append(const ChessState& st, const Workspace& ws, const void* k_rows, const void* v_rows,
-                  int64_t row_stride, const uint8_t* active, cudaStream_t stream) {
+                  int64_t row_stride, const uint8_t* active, cudaStream_t stream, int64_t col0,
+                  int64_t ncols, int post) {
+  if (ncols < 0) ncols = st.d.dim;
   const int64_t per = (int64_t)kNT * 8;
-  dim3 grid((unsigned)((st.d.dim + per - 1) / per), st.d.batch);
+  dim3 grid((unsigned)((ncols + per - 1) / per), st.d.batch);
   append_kernel<<<grid, kNT, 0, stream>>>(st, reinterpret_cast<const __nv_bfloat16*>(k_rows),
                                           reinterpret_cast<const __nv_bfloat16*>(v_rows),
-                                          row_stride, active, ws.append_done);
+                                          row_stride, active, ws.append_done, col0, ncols, post);
   return check_launch("append_kv");
 }
 
