@@ -15,7 +15,6 @@ token on the device, so a whole token is one capturable CUDA graph.
 
 from __future__ import annotations
 
-import ctypes as C
 import math
 from dataclasses import dataclass
 
@@ -75,17 +74,22 @@ class LlamaChess:
         self.inv_freq = 1.0 / (s.rope_theta ** (torch.arange(half, device=dev, dtype=torch.float32) / half))
 
     def _rms(self, x, wgt):
-        xf = x.float()
-        return (xf * torch.rsqrt(xf.pow(2).mean(-1, keepdim=True) + self.shape.eps)).to(torch.bfloat16) * wgt
+        return torch.nn.functional.rms_norm(x, (x.shape[-1],), wgt, self.shape.eps)
 
-    def _rope(self, x, pos):
-        # x [b, H, d] bf16, pos [b] (rotate-half convention)
+    def _rope_tables(self, pos):
+        """cos/sin [b, 1, d] of the rotate-half form, once per token step."""
         ang = pos.float()[:, None] * self.inv_freq[None, :]
-        cos, sin = ang.cos()[:, None, :], ang.sin()[:, None, :]
+        ang = torch.cat([ang, ang], dim=-1)[:, None, :]
+        return ang.cos(), ang.sin()
+
+    @staticmethod
+    def _rope(x, cs):
+        # x [b, H, d] bf16 (rotate-half convention)
+        cos, sin = cs
         xf = x.float()
         h = xf.shape[-1] // 2
-        x1, x2 = xf[..., :h], xf[..., h:]
-        return torch.cat([x1 * cos - x2 * sin, x2 * cos + x1 * sin], dim=-1).to(torch.bfloat16)
+        rot = torch.cat([-xf[..., h:], xf[..., :h]], dim=-1)
+        return (xf * cos + rot * sin).to(torch.bfloat16)
 
     def step(self, tokens, logits_out, next_tokens, stream=None):
         """tokens [b] int64 (device) -> logits_out [b, V] f32, next_tokens [b]
@@ -94,14 +98,14 @@ class LlamaChess:
         s, st, dec = self.shape, self.state, self.dec
         b = st.shape.batch
         sp = _lib.stream_ptr(stream)
-        pos = st.token_count.clone()  # position of the new token = tokens so far
+        cs = self._rope_tables(st.token_count)  # position of the new token = tokens so far
         x = self.embed[tokens]
         hq, hk, d = s.q_heads * s.head_dim, s.kv_heads * s.head_dim, s.head_dim
         for li, lw in enumerate(self.layers):
             h = self._rms(x, lw["n1"])
             qkv = h @ lw["wqkv"]
-            q = self._rope(qkv[:, :hq].view(b, s.q_heads, d), pos)
-            k = self._rope(qkv[:, hq:hq + hk].view(b, s.kv_heads, d), pos).reshape(b, hk).contiguous()
+            q = self._rope(qkv[:, :hq].view(b, s.q_heads, d), cs)
+            k = self._rope(qkv[:, hq:hq + hk].view(b, s.kv_heads, d), cs).reshape(b, hk).contiguous()
             v = qkv[:, hq + hk:].contiguous()
             _lib.call("chess_append_kv_layers", st.ref, li, li + 1, _lib.ptr(k), _lib.ptr(v), k.stride(0), None, sp)
             o = torch.empty((b, s.q_heads, d), dtype=torch.bfloat16, device=x.device)
@@ -132,19 +136,20 @@ class LlamaChess:
 
 def dense_reference_step(model: LlamaChess, kv_cache, tokens, pos):
     """Pure-torch fp32-attention restatement of one model step over a dense
-    per-slot K/V cache (test oracle for `policy="never"`, where the working
-    set is every page): kv_cache = list per layer of (K [b, T, H_kv, d], V)
+    per-slot K/V cache (test oracle while the working set is every page, e.g.
+    contexts the W-page window covers): kv_cache = list per layer of (K [b, T, H_kv, d], V)
     bf16, extended in place by one position.  Returns logits [b, V] f32."""
     s = model.shape
     b = tokens.shape[0]
     hq, hk, d = s.q_heads * s.head_dim, s.kv_heads * s.head_dim, s.head_dim
     gq = s.q_heads // s.kv_heads
+    cs = model._rope_tables(pos)
     x = model.embed[tokens]
     for li, lw in enumerate(model.layers):
         h = model._rms(x, lw["n1"])
         qkv = h @ lw["wqkv"]
-        q = model._rope(qkv[:, :hq].view(b, s.q_heads, d), pos)
-        k = model._rope(qkv[:, hq:hq + hk].view(b, s.kv_heads, d), pos)
+        q = model._rope(qkv[:, :hq].view(b, s.q_heads, d), cs)
+        k = model._rope(qkv[:, hq:hq + hk].view(b, s.kv_heads, d), cs)
         v = qkv[:, hq + hk:].view(b, s.kv_heads, d)
         K, V = kv_cache[li]
         K = torch.cat([K, k[:, None]], dim=1)
