@@ -83,3 +83,31 @@ def test_host_validation_before_launch(lib):
     assert lib.chess_working_set(None, 0, 4, 0, 1, None, None, None, None, None, None) == _lib.ERR_CONFIG
     assert lib.chess_entropy_probs(None, 1, 0, 0, None, None, None) == _lib.ERR_SHAPE
     assert "bad shape" in _lib.last_error()
+
+
+def test_config_struct_layouts_match_header(tmp_path):
+    """Field offsets of the by-pointer config structs, as gcc lays them out
+    from include/chess_b200.h, equal the ctypes mirror's."""
+    import shutil
+    import subprocess
+
+    if shutil.which("gcc") is None:
+        pytest.skip("gcc not available")
+    structs = {name: getattr(_lib, name) for name in
+               ("ChessSelectCfg", "ChessTriggerCfg", "ChessPeerExchange", "ChessPeerOutputs", "ChessDims")}
+    lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "chess_b200.h"', "int main(void) {"]
+    for name, cls in structs.items():
+        lines.append(f'  printf("{name} sizeof %zu\\n", sizeof({name}));')
+        for f in cls._fields_:
+            lines.append(f'  printf("{name} {f[0]} %zu\\n", offsetof({name}, {f[0]}));')
+    lines += ["  return 0;", "}"]
+    src = tmp_path / "layout.c"
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "layout"
+    subprocess.run(["gcc", "-std=c11", "-I", str(HEADER.parent), str(src), "-o", str(exe)], check=True)
+    out = subprocess.run([str(exe)], check=True, capture_output=True, text=True).stdout.split("\n")
+    for line in filter(None, out):
+        name, field, value = line.split()
+        cls = structs[name]
+        want = C.sizeof(cls) if field == "sizeof" else getattr(cls, field).offset
+        assert int(value) == want, (name, field, value, want)
