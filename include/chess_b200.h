@@ -201,10 +201,10 @@ int chess_reset_slots(const ChessState* st, const uint8_t* mask, void* stream);
 int chess_append_kv(const ChessState* st, const void* k_rows, const void* v_rows,
                     int64_t row_stride, const uint8_t* active, void* stream);
 
-/* The same append one layer range at a time, for a model that produces a
- * layer's K/V only after the previous layer's attention.  k_rows/v_rows:
- * bf16 [batch][row_stride] holding the columns of layers [layer_begin,
- * layer_end) only.  The call with layer_begin == 0 is the token's first: it
+/* The same append (kv_store.py:141-154) one layer range at a time, for a
+ * model that produces a layer's K/V only after the previous layer's
+ * attention.  k_rows/v_rows: bf16 [batch][row_stride] holding the columns of
+ * layers [layer_begin, layer_end) only.  The call with layer_begin == 0 is the token's first: it
  * opens the page and publishes the counters / block table exactly as
  * chess_append_kv (so layer 0's decode already sees the token); calls with
  * layer_begin > 0 write the same row of the same page.  Every layer must be
