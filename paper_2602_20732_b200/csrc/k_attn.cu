@@ -104,7 +104,11 @@ __device__ __forceinline__ void out_pair(const AttnArgs& a, __nv_bfloat16* orow,
   const __nv_bfloat162 v = __floats2bfloat162_rn(x, y);
   *reinterpret_cast<__nv_bfloat162*>(orow) = v;
   const int64_t off = orow - a.out;
-  for (int p = 0; p < a.n_peer; ++p) *reinterpret_cast<__nv_bfloat162*>(a.peer_out[p] + off) = v;
+  // constant indices only: a runtime index into the kernel-parameter array
+  // would copy AttnArgs to the local stack in every K4 instance
+#pragma unroll
+  for (int p = 0; p < kMaxPeers - 1; ++p)
+    if (p < a.n_peer) *reinterpret_cast<__nv_bfloat162*>(a.peer_out[p] + off) = v;
 }
 
 // Debug timeline (read by chess_debug_attn_trace): per CTA globaltimer stamps
