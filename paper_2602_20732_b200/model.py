@@ -104,16 +104,18 @@ class LlamaChess:
         for li, lw in enumerate(self.layers):
             h = self._rms(x, lw["n1"])
             qkv = h @ lw["wqkv"]
-            q = self._rope(qkv[:, :hq].view(b, s.q_heads, d), cs)
-            k = self._rope(qkv[:, hq:hq + hk].view(b, s.kv_heads, d), cs).reshape(b, hk).contiguous()
+            # q and k rotated together: [b, H_q + H_kv, d]
+            qk = self._rope(qkv[:, :hq + hk].view(b, s.q_heads + s.kv_heads, d), cs)
+            q = qk[:, :s.q_heads]
+            k = qk[:, s.q_heads:].reshape(b, hk).contiguous()  # k and v share one row stride
             v = qkv[:, hq + hk:].contiguous()
             _lib.call("chess_append_kv_layers", st.ref, li, li + 1, _lib.ptr(k), _lib.ptr(v), k.stride(0), None, sp)
             o = torch.empty((b, s.q_heads, d), dtype=torch.bfloat16, device=x.device)
-            dec.attend(li, q.contiguous(), o, None, stream)
-            x = x + o.view(b, hq) @ lw["wo"]
+            dec.attend(li, q, o, None, stream)
+            x = torch.addmm(x, o.view(b, hq), lw["wo"])
             h = self._rms(x, lw["n2"])
             gu = h @ lw["wgu"]
-            x = x + (torch.nn.functional.silu(gu[:, :s.ffn]) * gu[:, s.ffn:]) @ lw["wd"]
+            x = torch.addmm(x, torch.nn.functional.silu(gu[:, :s.ffn]) * gu[:, s.ffn:], lw["wd"])
         logits_out.copy_((self._rms(x, self.norm) @ self.lm_head).float())
         next_tokens.copy_(logits_out.argmax(-1))
         dec.entropy_trigger(logits_out, None, stream)
