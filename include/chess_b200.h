@@ -192,7 +192,8 @@ size_t chess_workspace_bytes(const ChessDims* d);
 int chess_reset_slots(const ChessState* st, const uint8_t* mask, void* stream);
 
 /* Append one token's K/V row per active slot (kv_store.py:141-154).
- * k_rows/v_rows: bf16 [batch][row_stride], flattened (layer, kv_head, d).
+ * k_rows/v_rows: bf16 [batch][row_stride] (one stride for both), flattened
+ * (layer, kv_head, d).
  * Opens the pre-reserved page page_table[s][num_pages[s]] when the tail is
  * sealed (allocation is host-side, kv_store.py:127-136), accumulates the f64
  * running key sum, sets sealed[s], and rebuilds the block table when a page
@@ -203,8 +204,8 @@ int chess_append_kv(const ChessState* st, const void* k_rows, const void* v_rows
 
 /* The same append (kv_store.py:141-154) one layer range at a time, for a
  * model that produces a layer's K/V only after the previous layer's
- * attention.  k_rows/v_rows: bf16 [batch][row_stride] holding the columns of
- * layers [layer_begin, layer_end) only.  The call with layer_begin == 0 is the token's first: it
+ * attention.  k_rows/v_rows: bf16 [batch][row_stride] (one stride for both)
+ * holding the columns of layers [layer_begin, layer_end) only.  The call with layer_begin == 0 is the token's first: it
  * opens the page and publishes the counters / block table exactly as
  * chess_append_kv (so layer 0's decode already sees the token); calls with
  * layer_begin > 0 write the same row of the same page.  Every layer must be
