@@ -99,16 +99,22 @@ struct AttnArgs {
   int mode;  // debug (CHESS_ATTN_MODE): 0 normal, 1 loads only (no math), 2 math only (no K/V loads), 5 exit at entry, 6 exit after the prologue, 7 force stream-K, 8 no PDL wait (timing only: ignores the previous kernel)
 };
 
-// one bf16 pair of an output row, to this rank's buffer and every peer's
+// one bf16 pair of an output row, to this rank's buffer and (PEERS: the
+// head-shard gather instance of K4) every peer's.  A compile-time switch: the
+// predicated peer stores kept their addresses live across the unrolled
+// epilogue (+10 registers in the cluster instance, 0.3-2.8% per step) even
+// with no peers.  Constant indices only: a runtime index into the
+// kernel-parameter array would copy AttnArgs to the local stack.
+template <bool PEERS>
 __device__ __forceinline__ void out_pair(const AttnArgs& a, __nv_bfloat16* orow, float x, float y) {
   const __nv_bfloat162 v = __floats2bfloat162_rn(x, y);
   *reinterpret_cast<__nv_bfloat162*>(orow) = v;
-  const int64_t off = orow - a.out;
-  // constant indices only: a runtime index into the kernel-parameter array
-  // would copy AttnArgs to the local stack in every K4 instance
+  if constexpr (PEERS) {
+    const int64_t off = orow - a.out;
 #pragma unroll
-  for (int p = 0; p < kMaxPeers - 1; ++p)
-    if (p < a.n_peer) *reinterpret_cast<__nv_bfloat162*>(a.peer_out[p] + off) = v;
+    for (int p = 0; p < kMaxPeers - 1; ++p)
+      if (p < a.n_peer) *reinterpret_cast<__nv_bfloat162*>(a.peer_out[p] + off) = v;
+  }
 }
 
 // Debug timeline (read by chess_debug_attn_trace): per CTA globaltimer stamps
@@ -270,7 +276,7 @@ __device__ __forceinline__ void st_release_cta(int* p, int v) {
 // arrives on the leader's mbarrier (release.cluster); the leader merges the
 // states in cluster-rank order.  This replaces the split-segment path's
 // global partials + fences + atomics (~3 us of round trips) on small batches.
-template <int HD, int GQ, int B, bool XC, int CPS>
+template <int HD, int GQ, int B, bool XC, int CPS, bool PEERS>
 __global__ void __launch_bounds__(kThreads, CPS)
     sparse_decode_kernel(ChessState st, Workspace ws, AttnArgs args,
                          const __grid_constant__ CUtensorMap kmap,
@@ -783,7 +789,7 @@ __global__ void __launch_bounds__(kThreads, CPS)
         __nv_bfloat16* orow = args.out + (int64_t)s * args.out_stride + ((int64_t)h * GQ + hh) * HD + el;
 #pragma unroll
         for (int e = 0; e < kE; e += 2)
-          out_pair(args, orow + e, acc[e] * inv, acc[e + 1] * inv);
+          out_pair<PEERS>(args, orow + e, acc[e] * inv, acc[e + 1] * inv);
         if (args.lse && el == 0) args.lse[(int64_t)s * d.q_heads + h * GQ + hh] = (Mx + log2f(Lx)) * kLn2;
       }
       u = piece_end;
@@ -886,14 +892,14 @@ __global__ void __launch_bounds__(kThreads, CPS)
           const float inv = 1.f / Lx;
 #pragma unroll
           for (int e = 0; e < C::kEPL; e += 2)
-            out_pair(args, orow + e, acc[e] * inv, acc[e + 1] * inv);
+            out_pair<PEERS>(args, orow + e, acc[e] * inv, acc[e + 1] * inv);
           if (lse && el == 0) *lse = (Mx + log2f(Lx)) * kLn2;
         }
       } else if (whole) {
         const float inv = 1.f / L;
 #pragma unroll
         for (int e = 0; e < C::kEPL; e += 2)
-          out_pair(args, orow + e, acc[e] * inv, acc[e + 1] * inv);
+          out_pair<PEERS>(args, orow + e, acc[e] * inv, acc[e + 1] * inv);
         if (lse && el == 0) *lse = (M + log2f(L)) * kLn2;
       } else {
         // split segment: partial (2*cta + which), which = 0 for the CTA's first piece
@@ -968,7 +974,7 @@ __global__ void __launch_bounds__(kThreads, CPS)
           const float inv = 1.f / Lx;
 #pragma unroll
           for (int e = 0; e < C::kEPL; e += 2)
-            out_pair(args, orow + e, ax[e] * inv, ax[e + 1] * inv);
+            out_pair<PEERS>(args, orow + e, ax[e] * inv, ax[e + 1] * inv);
           if (lse && el == 0) *lse = (Mx + log2f(Lx)) * kLn2;
           if (lane == 0) ws.attn_done[sg] = 0;
         }
@@ -1023,7 +1029,9 @@ template <int HD, int GQ, int B>
 int launch_cluster(const ChessState& st, const Workspace& ws, const AttnArgs& args, int segs,
                    cudaStream_t stream) {
   using C = Cfg<HD, GQ, B, true>;
-  auto kfn = sparse_decode_kernel<HD, GQ, B, true, 1>;  // smem attribute set by cluster_size_for
+  // smem attributes of both instances set by cluster_size_for
+  auto kfn = args.n_peer ? sparse_decode_kernel<HD, GQ, B, true, 1, true>
+                         : sparse_decode_kernel<HD, GQ, B, true, 1, false>;
   CUtensorMap km, vm;
   int rc = make_kv_map(&km, st.k_pool, st.d);
   if (rc) return rc;
@@ -1057,10 +1065,24 @@ template <int HD, int GQ, int B>
 int cluster_size_for(int segs) {
   static int max_active[kMaxCluster + 1] = {};
   static bool probed = false;
-  auto kfn = sparse_decode_kernel<HD, GQ, B, true, 1>;
+  auto kfn = sparse_decode_kernel<HD, GQ, B, true, 1, false>;
   using C = Cfg<HD, GQ, B, true>;
   if (!probed) {
+    // Load every instance of this shape now (first launch of the shape):
+    // with CUDA's lazy module loading a kernel's first launch can wait for
+    // running kernels, so a first launch of the peer-store instance while a
+    // peer-exchange wait spins on the same device (in-process multi-rank
+    // runs) would stall until the wait times out.
+    cudaFuncAttributes fa;
+    cudaFuncGetAttributes(&fa, sparse_decode_kernel<HD, GQ, B, true, 1, false>);
+    cudaFuncGetAttributes(&fa, sparse_decode_kernel<HD, GQ, B, true, 1, true>);
+    cudaFuncGetAttributes(&fa, sparse_decode_kernel<HD, GQ, B, false, 1, false>);
+    cudaFuncGetAttributes(&fa, sparse_decode_kernel<HD, GQ, B, false, 1, true>);
+    cudaFuncGetAttributes(&fa, sparse_decode_kernel<HD, GQ, B, false, 2, false>);
+    cudaFuncGetAttributes(&fa, sparse_decode_kernel<HD, GQ, B, false, 2, true>);
     cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::kSmem);
+    cudaFuncSetAttribute(sparse_decode_kernel<HD, GQ, B, true, 1, true>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::kSmem);
     for (int cl = 2; cl <= kMaxCluster; cl *= 2) {
       cudaLaunchConfig_t cfg = {};
       cfg.gridDim = dim3(cl * 8);
@@ -1114,9 +1136,13 @@ int launch_grid(const ChessState& st, const Workspace& ws, const AttnArgs& args,
   using C = Cfg<HD, GQ, B, false, CPS>;
   const size_t smem = C::kSmem;
   static bool configured = false;
-  auto kfn = sparse_decode_kernel<HD, GQ, B, false, CPS>;
+  auto kfn = args.n_peer ? sparse_decode_kernel<HD, GQ, B, false, CPS, true>
+                         : sparse_decode_kernel<HD, GQ, B, false, CPS, false>;
   if (!configured) {
-    cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(sparse_decode_kernel<HD, GQ, B, false, CPS, false>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(sparse_decode_kernel<HD, GQ, B, false, CPS, true>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     configured = true;
   }
   CUtensorMap km, vm;
