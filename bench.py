@@ -284,7 +284,7 @@ def run_gpu(args):
     with torch.cuda.graph(g_attn, stream=gs):
         for _ in range(reps):
             for layer in range(L):
-                dec.attend(layer, q[:, layer], wl.out[:, layer], stream=gs)
+                dec.attend(layer, q[:, layer], wl.out[:, layer], stream=gs, after_decode=layer > 0)
     with torch.cuda.graph(g_sel, stream=gs):
         for _ in range(reps):
             dec.select(force_all=True, stream=gs)

@@ -32,7 +32,7 @@
 extern "C" {
 #endif
 
-#define CHESS_ABI_VERSION 4
+#define CHESS_ABI_VERSION 5
 
 /* Status codes.  Python shim maps them to the pagesel exception classes
  * (pagesel/errors.py:4-21 and the ValueError/IndexError sites listed). */
@@ -79,7 +79,7 @@ typedef struct ChessDims {
   int32_t chunks_per_grid; /* N_g (config.py:29)                               */
   int32_t max_pages;       /* per-sequence page-table / index capacity         */
   int32_t window_pages;    /* W   (config.py:33)                               */
-  int32_t max_ws;          /* block-table row capacity                         */
+  int32_t max_ws;          /* block-table row capacity (>= max_pages)          */
   int32_t summary_dtype;   /* 0: scan float32 mirrors, 1: scan float64,
                             * 2: scan bf16 mirrors (held in the *_vec32 buffers) */
   int64_t dim;             /* D                                                */
@@ -336,7 +336,7 @@ typedef struct ChessPeerOutputs {
 } ChessPeerOutputs;
 int chess_sparse_decode_gather(const ChessState* st, int32_t layer, const void* q, int64_t q_stride,
                                void* out, int64_t out_stride, float* lse, float softmax_scale,
-                               const ChessPeerOutputs* po, void* stream);
+                               uint32_t flags, const ChessPeerOutputs* po, void* stream);
 int chess_gather_finish(const ChessState* st, const ChessPeerOutputs* po, void* out, void* stream);
 #define CHESS_IPC_HANDLE_BYTES 64
 int chess_p2p_alloc(int64_t bytes, void** ptr);           /* zeroed device memory */
@@ -360,6 +360,19 @@ int chess_flush_working_sets(const ChessState* st, void* stream);
 int chess_sparse_decode(const ChessState* st, int32_t layer, const void* q, int64_t q_stride,
                         void* out, int64_t out_stride, float* lse, float softmax_scale,
                         void* stream);
+
+/* Launch-ordering flags of chess_sparse_decode_ex / _gather.  K4 is launched
+ * with programmatic dependent launch.  CHESS_ATTN_AFTER_DECODE promises that
+ * the kernel before it on the stream is another chess_sparse_decode (which
+ * writes only out/lse), so K4 may read the block table, ws_len, tail_fill and
+ * the first K/V pages before griddepcontrol.wait and overlap that kernel's
+ * tail.  Without it (chess_sparse_decode, flags 0) K4 waits for the previous
+ * kernel's writes before reading any state — required after chess_append_kv*,
+ * which writes the token's K/V row, tail_fill and (page open) the block table. */
+#define CHESS_ATTN_AFTER_DECODE 1u
+int chess_sparse_decode_ex(const ChessState* st, int32_t layer, const void* q, int64_t q_stride,
+                           void* out, int64_t out_stride, float* lse, float softmax_scale,
+                           uint32_t flags, void* stream);
 
 /* K5: entropy of each slot's next-token distribution from fp32 logits
  * (entropy of softmax, uncertainty.py:22-31), appended to the open page's
@@ -391,7 +404,8 @@ int chess_mean_rows(const void* rows, int32_t dtype, int64_t n_rows, int64_t dim
 /* hierarchical_prune with arbitrary parent maps (selection.py:91-111).
  * Writes the kept pages in increasing order to out_pages and their count to
  * out_count[0]; out_count[1..2] = kept grids, kept chunks.  workspace >=
- * 16*(G + C + P) bytes. */
+ * chess_prune_workspace_bytes(G, C, P) = 16*(G + C + P) + 4*(G + C) bytes. */
+size_t chess_prune_workspace_bytes(int32_t G, int32_t C, int32_t P);
 int chess_prune(const double* s_g, int32_t G, const double* s_c, int32_t C, const double* s_p,
                 int32_t P, const int64_t* page_to_chunk, const int64_t* chunk_to_grid,
                 double rho_grid, double rho_chunk, double rho_page, int32_t* out_pages,

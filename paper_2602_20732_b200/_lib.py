@@ -21,7 +21,7 @@ from .errors import (
 )
 
 LIB_PATH = Path(__file__).resolve().parent / "libchess_b200.so"
-ABI_VERSION = 4
+ABI_VERSION = 5
 
 # enum ChessStatus
 OK, ERR_CONFIG, ERR_OUT_OF_PAGES, ERR_EMPTY_CONTEXT, ERR_SHAPE, ERR_INDEX, ERR_ORDER, ERR_VALUE, ERR_CUDA, ERR_UNSUPPORTED = range(10)
@@ -125,6 +125,10 @@ _I32 = C.c_int32
 _I64 = C.c_int64
 _D = C.c_double
 _F = C.c_float
+_U32 = C.c_uint32
+
+# launch-ordering flag of chess_sparse_decode_ex (include/chess_b200.h)
+ATTN_AFTER_DECODE = 1
 
 # name -> (restype, argtypes).  Exactly the symbols declared in include/chess_b200.h.
 SIGNATURES = {
@@ -152,7 +156,7 @@ SIGNATURES = {
     "chess_select_pull": (C.c_int, [C.POINTER(ChessState), C.POINTER(ChessSelectCfg), _I32,
                                     C.POINTER(ChessPeerExchange), _P]),
     "chess_sparse_decode_gather": (C.c_int, [C.POINTER(ChessState), _I32, _P, _I64, _P, _I64, _P, _F,
-                                             C.POINTER(ChessPeerOutputs), _P]),
+                                             _U32, C.POINTER(ChessPeerOutputs), _P]),
     "chess_gather_finish": (C.c_int, [C.POINTER(ChessState), C.POINTER(ChessPeerOutputs), _P, _P]),
     "chess_p2p_alloc": (C.c_int, [_I64, C.POINTER(C.c_void_p)]),
     "chess_p2p_free": (C.c_int, [_P]),
@@ -162,11 +166,13 @@ SIGNATURES = {
     "chess_build_working_set": (C.c_int, [C.POINTER(ChessState), _P]),
     "chess_flush_working_sets": (C.c_int, [C.POINTER(ChessState), _P]),
     "chess_sparse_decode": (C.c_int, [C.POINTER(ChessState), _I32, _P, _I64, _P, _I64, _P, _F, _P]),
+    "chess_sparse_decode_ex": (C.c_int, [C.POINTER(ChessState), _I32, _P, _I64, _P, _I64, _P, _F, _U32, _P]),
     "chess_entropy_trigger": (C.c_int, [C.POINTER(ChessState), _P, _I64, _I64, C.POINTER(ChessTriggerCfg), _P, _P]),
     "chess_record_entropy": (C.c_int, [C.POINTER(ChessState), _P, _P, C.POINTER(ChessTriggerCfg), _P]),
     "chess_score_rows": (C.c_int, [_P, _I32, _I64, _I64, _I64, _P, _P, _P]),
     "chess_mean_rows": (C.c_int, [_P, _I32, _I64, _I64, _I64, _P, _P]),
     "chess_prune": (C.c_int, [_P, _I32, _P, _I32, _P, _I32, _P, _P, _D, _D, _D, _P, _P, _P, _P]),
+    "chess_prune_workspace_bytes": (C.c_size_t, [_I32, _I32, _I32]),
     "chess_topk": (C.c_int, [_P, _I32, _I32, _P, _P, _P, _I32, _P, _P]),
     "chess_working_set": (C.c_int, [_P, _I32, _I32, _I32, _I32, _P, _P, _P, _P, _P, _P]),
     "chess_gather_pages": (C.c_int, [_P, _I32, _P, _I32, _P, _P, _P]),

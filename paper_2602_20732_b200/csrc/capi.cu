@@ -44,7 +44,7 @@ int launch_working_set(const int32_t*, int, int, int, int, const int32_t*, int32
 int launch_gather_pages(const int32_t*, int, const int64_t*, int, int32_t*, int32_t*,
                         cudaStream_t);
 int launch_sparse_decode(const ChessState&, const Workspace&, int, const void*, int64_t, void*,
-                         int64_t, float*, float, cudaStream_t, const PeerOut* = nullptr);
+                         int64_t, float*, float, uint32_t, cudaStream_t, const PeerOut* = nullptr);
 int launch_gather_finish(uint32_t* const*, uint32_t*, int, int, uint32_t*, int32_t*, const void*, int64_t,
                          int64_t, void*, cudaStream_t);
 int launch_entropy_trigger(const ChessState&, const Workspace&, const float*, int64_t, int64_t,
@@ -166,6 +166,12 @@ static int validate(const ChessDims& d) {
   if (d.summary_dtype == 2 && d.ld % 8)
     return fail(CHESS_ERR_CONFIG, "bf16 summary mirrors need ld %% 8 == 0 (16-byte rows for the bulk copies)");
   if (d.max_pages < 1 || d.max_ws < 1) return fail(CHESS_ERR_CONFIG, "max_pages/max_ws must be >= 1");
+  // a working set can hold every page of the table (policy 'never' keeps all
+  // sealed pages, plus the open tail); a shorter block-table row would cut
+  // the window / tail entries K4 relies on
+  if (d.max_ws < d.max_pages)
+    return fail(CHESS_ERR_CONFIG, "max_ws (%d) must be >= max_pages (%d): a working set may hold every page",
+                d.max_ws, d.max_pages);
   if (d.n_phys < 1) return fail(CHESS_ERR_CONFIG, "store capacity must be >= 1 page");
   if (d.summary_dtype < 0 || d.summary_dtype > 2) return fail(CHESS_ERR_CONFIG, "summary_dtype must be 0 (f32), 1 (f64) or 2 (bf16)");
   return CHESS_OK;
@@ -481,6 +487,12 @@ int chess_build_working_set(const ChessState* st, void* stream) {
 int chess_sparse_decode(const ChessState* st, int32_t layer, const void* q, int64_t q_stride,
                         void* out, int64_t out_stride, float* lse, float softmax_scale,
                         void* stream) {
+  return chess_sparse_decode_ex(st, layer, q, q_stride, out, out_stride, lse, softmax_scale, 0u, stream);
+}
+
+int chess_sparse_decode_ex(const ChessState* st, int32_t layer, const void* q, int64_t q_stride,
+                           void* out, int64_t out_stride, float* lse, float softmax_scale,
+                           uint32_t flags, void* stream) {
   Workspace ws;
   int rc = state_ws(st, &ws);
   if (rc) return rc;
@@ -488,7 +500,8 @@ int chess_sparse_decode(const ChessState* st, int32_t layer, const void* q, int6
   if (!q || !out) return fail(CHESS_ERR_SHAPE, "sparse_decode: null q/out");
   const int64_t row = (int64_t)st->d.q_heads * st->d.head_dim;
   if (q_stride < row || out_stride < row) return fail(CHESS_ERR_SHAPE, "sparse_decode: stride < q_heads*head_dim");
-  return launch_sparse_decode(*st, ws, layer, q, q_stride, out, out_stride, lse, softmax_scale,
+  if (flags & ~(uint32_t)CHESS_ATTN_AFTER_DECODE) return fail(CHESS_ERR_CONFIG, "sparse_decode: unknown flags %#x", flags);
+  return launch_sparse_decode(*st, ws, layer, q, q_stride, out, out_stride, lse, softmax_scale, flags,
                               (cudaStream_t)stream);
 }
 
@@ -510,7 +523,7 @@ static int64_t gather_block(const ChessDims& d) { return (int64_t)d.batch * d.q_
 
 int chess_sparse_decode_gather(const ChessState* st, int32_t layer, const void* q, int64_t q_stride,
                                void* out, int64_t out_stride, float* lse, float softmax_scale,
-                               const ChessPeerOutputs* po, void* stream) {
+                               uint32_t flags, const ChessPeerOutputs* po, void* stream) {
   Workspace ws;
   int rc = state_ws(st, &ws);
   if (rc) return rc;
@@ -527,8 +540,10 @@ int chess_sparse_decode_gather(const ChessState* st, int32_t layer, const void* 
   pe.n_peer = 0;
   for (int p = 0; p < po->world; ++p)
     if (p != po->rank) pe.peer_out[pe.n_peer++] = static_cast<__nv_bfloat16*>(po->regions[p]) + off;
-  return launch_sparse_decode(*st, ws, layer, q, q_stride, out, row, lse, softmax_scale, (cudaStream_t)stream,
-                              &pe);
+  if (flags & ~(uint32_t)CHESS_ATTN_AFTER_DECODE)
+    return fail(CHESS_ERR_CONFIG, "sparse_decode_gather: unknown flags %#x", flags);
+  return launch_sparse_decode(*st, ws, layer, q, q_stride, out, row, lse, softmax_scale, flags,
+                              (cudaStream_t)stream, &pe);
 }
 
 int chess_gather_finish(const ChessState* st, const ChessPeerOutputs* po, void* out, void* stream) {
@@ -566,6 +581,13 @@ int chess_mean_rows(const void* rows, int32_t dtype, int64_t n_rows, int64_t dim
   if (dim < 0 || ld < dim) return fail(CHESS_ERR_SHAPE, "mean_rows: bad shape");
   if (dim == 0) return CHESS_OK;
   return launch_mean_rows(rows, dtype, n_rows, dim, ld, out, (cudaStream_t)stream);
+}
+
+size_t chess_prune_workspace_bytes(int32_t G, int32_t C, int32_t P) {
+  if (G < 0 || C < 0 || P < 0) return 0;
+  // keys (8 B) + kept (4 B) + cand (4 B) per candidate, then the kept-grid /
+  // kept-chunk masks (4 B each) — prune_kernel's layout
+  return 16 * ((size_t)G + C + P) + 4 * ((size_t)G + C);
 }
 
 int chess_prune(const double* s_g, int32_t G, const double* s_c, int32_t C, const double* s_p,

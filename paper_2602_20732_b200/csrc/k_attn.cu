@@ -96,6 +96,10 @@ struct AttnArgs {
   // (this rank's block in peer p's region, NVLink stores).
   __nv_bfloat16* peer_out[kMaxPeers - 1];
   int n_peer;
+  int early;  // 1: the previous kernel on the stream is a K4 (CHESS_ATTN_AFTER_DECODE), which
+              // writes none of the state the prologue reads, so the prologue and the first
+              // K/V loads may run before griddepcontrol.wait; 0: wait first (e.g. after an
+              // append, which writes the tail row, tail_fill and the block table)
   int mode;  // debug (CHESS_ATTN_MODE): 0 normal, 1 loads only (no math), 2 math only (no K/V loads), 5 exit at entry, 6 exit after the prologue, 7 force stream-K, 8 no PDL wait (timing only: ignores the previous kernel)
 };
 
@@ -316,11 +320,15 @@ __global__ void __launch_bounds__(kThreads, CPS)
       for (int i = 0; i < 16; ++i) g_attn_trace[args.layer & 1][blockIdx.x][i] = 0;
   }
   if (args.mode == 5) return;  // debug: launch overhead only
-  // Everything up to the q load reads state that was final before the
-  // previous kernel started (KV pool, block table, ws_len, fill), so the
-  // prologue, the block-table fetch and the first K/V TMA loads overlap the
-  // previous kernel's tail under PDL; griddepcontrol.wait guards the q reads
-  // and every write (out, lse, split partials, counters).
+  // After another K4 (args.early), everything up to the q load reads state
+  // that was final before the previous kernel started (KV pool, block table,
+  // ws_len, fill), so the prologue, the block-table fetch and the first K/V
+  // TMA loads overlap the previous kernel's tail under PDL; griddepcontrol.wait
+  // guards the q reads and every write (out, lse, split partials, counters).
+  // Any other predecessor (an append writes the token's K/V row, tail_fill and
+  // the block table) may not have made its writes visible before the wait, so
+  // the kernel waits before reading anything.
+  if (!args.early && args.mode != 8) pdl_wait();
   // pages per segment: np = ws_len - 1 + (fill > 0); prefix over slots (x H)
   if (warp == 0) {
     int run = 0;
@@ -1174,9 +1182,10 @@ int attn_ctas_for(const ChessDims& d) {
 
 int launch_sparse_decode(const ChessState& st, const Workspace& ws, int layer, const void* q,
                          int64_t q_stride, void* out, int64_t out_stride, float* lse,
-                         float softmax_scale, cudaStream_t stream, const PeerOut* po) {
+                         float softmax_scale, uint32_t flags, cudaStream_t stream, const PeerOut* po) {
   const ChessDims& d = st.d;
   AttnArgs a;
+  a.early = (flags & CHESS_ATTN_AFTER_DECODE) ? 1 : 0;
   a.n_peer = 0;
   if (po) {
     a.n_peer = po->n_peer;

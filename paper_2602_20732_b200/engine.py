@@ -195,11 +195,17 @@ class ChessDecoder:
             k_new.stride(0), None, _lib.stream_ptr(stream),
         )
 
-    def attend(self, layer, q, out, lse=None, stream=None):
-        """K4 for one layer: q/out [batch, q_heads, head_dim] (batch stride may be padded)."""
+    def attend(self, layer, q, out, lse=None, stream=None, after_decode=False):
+        """K4 for one layer: q/out [batch, q_heads, head_dim] (batch stride may be padded).
+
+        after_decode: the previous kernel on `stream` writes none of the state
+        K4 reads (another K4, or a collective on the outputs), so K4's prologue
+        and first page loads may overlap it (CHESS_ATTN_AFTER_DECODE).  False
+        after an append, whose writes K4 must wait for."""
         _lib.call(
-            "chess_sparse_decode", self.state.ref, layer, _lib.ptr(q), q.stride(0),
-            _lib.ptr(out), out.stride(0), _lib.ptr(lse), self.scale, _lib.stream_ptr(stream),
+            "chess_sparse_decode_ex", self.state.ref, layer, _lib.ptr(q), q.stride(0),
+            _lib.ptr(out), out.stride(0), _lib.ptr(lse), self.scale,
+            _lib.ATTN_AFTER_DECODE if after_decode else 0, _lib.stream_ptr(stream),
         )
 
     def entropy_trigger(self, logits, entropy_out=None, stream=None):
@@ -231,12 +237,13 @@ class ChessDecoder:
             sp = _lib.stream_ptr(stream)
             for layer in range(self.state.shape.layers):
                 x.attend(self.state, layer, q[:, layer], out[layer, x.rank], None if lse is None else lse[layer],
-                         self.scale, sp)
+                         self.scale, sp, after_decode=layer > 0)
             x.finish_outputs(self.state, out, sp)
         else:
             for layer in range(self.state.shape.layers):
                 o = out[:, layer] if x is None else out[layer, x.rank]
-                self.attend(layer, q[:, layer], o, None if lse is None else lse[layer], stream)
+                self.attend(layer, q[:, layer], o, None if lse is None else lse[layer], stream,
+                            after_decode=layer > 0)
                 if x is not None:
                     with _on(stream):
                         x.outputs(out[layer])
@@ -260,7 +267,8 @@ class ChessDecoder:
         self.seal(side)
         self.select(force_all=False, stream=side, defer_ws=True)
         for layer in range(self.state.shape.layers):
-            self.attend(layer, q[:, layer], out[:, layer], None if lse is None else lse[layer], cur)
+            self.attend(layer, q[:, layer], out[:, layer], None if lse is None else lse[layer], cur,
+                        after_decode=layer > 0)
         join = torch.cuda.Event()
         join.record(side)
         cur.wait_event(join)

@@ -92,13 +92,44 @@ class AppendEvent:
     logical_index: int
 
 
+class ReadOnlyRows(torch.Tensor):
+    """A CUDA view whose writes raise ValueError, like the reference's
+    read-only NumPy views of a page's rows (kv_store.py:52-65): item
+    assignment and in-place ops raise, views of it stay read-only, and
+    computed results are plain tensors.  `copy()` and `__array__` give host
+    NumPy arrays, so `np.array_equal(page.keys, first)` works as there."""
+
+    @classmethod
+    def __torch_function__(cls, func, types, args=(), kwargs=None):
+        name = getattr(func, "__name__", "")
+        if name == "__setitem__" or (name.endswith("_") and not name.startswith("_")):
+            raise ValueError("assignment destination is read-only")
+        with torch._C.DisableTorchFunctionSubclass():
+            out = func(*args, **(kwargs or {}))
+        src = args[0] if args and isinstance(args[0], torch.Tensor) else None
+        if isinstance(out, torch.Tensor) and not isinstance(out, ReadOnlyRows):
+            shares = src is not None and out.numel() and src.numel() and \
+                out.untyped_storage().data_ptr() == src.untyped_storage().data_ptr()
+            if shares:
+                out = out.as_subclass(ReadOnlyRows)
+        return out
+
+    def copy(self):
+        return self.detach().cpu().numpy().copy()
+
+    def __array__(self, dtype=None, copy=None):
+        a = self.detach().cpu().numpy()
+        return a.astype(dtype) if dtype is not None else a
+
+
 class KvPage:
     """One physical page of the device pool (kv_store.py:29-74).  `keys` /
-    `values` are CUDA float64 views of the filled rows."""
+    `values` are read-only CUDA float64 views of the filled rows."""
 
-    def __init__(self, store, page_id):
+    def __init__(self, store, page_id, slot=None):
         self._store = store
         self.page_id = page_id
+        self._slot = page_id if slot is None else slot  # row block of the pool
         self.page_size = store.page_size
         self.fill = 0
         self.version = 0
@@ -110,25 +141,25 @@ class KvPage:
     def write(self, key, value):
         if self.sealed:
             raise ValueError(f"page {self.page_id} is sealed")
-        self._store._keys[self.page_id, self.fill].copy_(_f64(key, self._store.device))
-        self._store._values[self.page_id, self.fill].copy_(_f64(value, self._store.device))
+        self._store._keys[self._slot, self.fill].copy_(_f64(key, self._store.device))
+        self._store._values[self._slot, self.fill].copy_(_f64(value, self._store.device))
         self.fill += 1
         self.version += 1
 
     @property
     def keys(self) -> torch.Tensor:
-        return self._store._keys[self.page_id, : self.fill]
+        return self._store._keys[self._slot, : self.fill].as_subclass(ReadOnlyRows)
 
     @property
     def values(self) -> torch.Tensor:
-        return self._store._values[self.page_id, : self.fill]
+        return self._store._values[self._slot, : self.fill].as_subclass(ReadOnlyRows)
 
     def dump(self):
         return {
             "page_id": self.page_id,
             "fill": self.fill,
-            "keys": self.keys.cpu().numpy().ravel().tolist(),
-            "values": self.values.cpu().numpy().ravel().tolist(),
+            "keys": self.keys.copy().ravel().tolist(),
+            "values": self.values.copy().ravel().tolist(),
         }
 
 
@@ -202,11 +233,15 @@ class PagedKvStore:
         return {pid: self._pages[pid].version for pid in seq.page_table if self._pages[pid].sealed}
 
 
-def page_from_record(record, store):
-    """Rebuild a page of `store` from a dump() record (fixture path)."""
-    page = store._allocate()
-    keys = np.asarray(record["keys"], dtype=np.float64).reshape(record["fill"], store.dim)
-    values = np.asarray(record["values"], dtype=np.float64).reshape(record["fill"], store.dim)
+def page_from_record(record, page_size, dim, device=None):
+    """Rebuild a KvPage from a dump() record (kv_store.py:67-74, test-fixture
+    path): a standalone page holding the record's rows, keeping its page_id."""
+    store = PagedKvStore(1, dim, page_size=page_size, device=device)
+    page = KvPage(store, record["page_id"], slot=0)
+    store._free.clear()
+    store._pages[page.page_id] = page
+    keys = np.asarray(record["keys"], dtype=np.float64).reshape(record["fill"], dim)
+    values = np.asarray(record["values"], dtype=np.float64).reshape(record["fill"], dim)
     for k, v in zip(keys, values):
         page.write(k, v)
     return page
@@ -248,7 +283,7 @@ class HierarchyIndex:
     def _make_state(self, max_pages):
         shape = Shape(batch=1, layers=1, kv_heads=1, q_heads=1, head_dim=self.dim, page_size=1,
                       pages_per_chunk=self.pages_per_chunk, chunks_per_grid=self.chunks_per_grid,
-                      max_pages=max_pages, window_pages=1, max_ws=1, n_phys=1, summary_dtype="f64")
+                      max_pages=max_pages, window_pages=1, max_ws=max_pages, n_phys=1, summary_dtype="f64")
         st = DecodeState(shape, device=self.device)
         st.reset()
         return st
@@ -449,7 +484,7 @@ def hierarchical_prune(s_g, s_c, s_p, page_to_chunk, chunk_to_grid, config):
     p2c, c2g = _i64(page_to_chunk, sp.device), _i64(chunk_to_grid, sp.device)
     out = torch.empty(P, dtype=torch.int32, device=sp.device)
     cnt = torch.zeros(3, dtype=torch.int32, device=sp.device)
-    ws = torch.empty(16 * (G + Cn + P) + 64, dtype=torch.uint8, device=sp.device)
+    ws = torch.empty(_lib.load().chess_prune_workspace_bytes(G, Cn, P), dtype=torch.uint8, device=sp.device)
     _lib.call("chess_prune", _lib.ptr(sg), G, _lib.ptr(sc), Cn, _lib.ptr(sp), P, _lib.ptr(p2c), _lib.ptr(c2g),
               config.rho_grid, config.rho_chunk, config.rho_page, _lib.ptr(out), _lib.ptr(cnt), _lib.ptr(ws), _sp())
     k = int(cnt[0].item())

@@ -267,7 +267,7 @@ class PeerScoreExchange(HeadShardExchange):
             self.po = _lib.ChessPeerOutputs(self.world, self.rank, self._regions, oflags.data_ptr(),
                                             self.base + fo, self.out_gen.data_ptr(), self.err.data_ptr())
 
-    def attend(self, state, layer, q, out, lse, scale, stream_ptr) -> None:
+    def attend(self, state, layer, q, out, lse, scale, stream_ptr, after_decode=False) -> None:
         """K4 for one layer: output rows into `out` (this rank's [layer, rank]
         block, [b, H_q/n, d] contiguous) and into every peer's region."""
         import ctypes as C
@@ -275,7 +275,8 @@ class PeerScoreExchange(HeadShardExchange):
         from . import _lib
 
         _lib.call("chess_sparse_decode_gather", state.ref, layer, _lib.ptr(q), q.stride(0), _lib.ptr(out),
-                  out.stride(0), _lib.ptr(lse), scale, C.byref(self.po), stream_ptr)
+                  out.stride(0), _lib.ptr(lse), scale, _lib.ATTN_AFTER_DECODE if after_decode else 0,
+                  C.byref(self.po), stream_ptr)
 
     def finish_outputs(self, state, out, stream_ptr) -> None:
         """Publish this rank's step, wait for every rank's, copy the peers'
