@@ -377,6 +377,8 @@ class Step:
     selection_ops: int
     attention_ops: int
     working_set: list = field(default_factory=list)
+    semantic: list = field(default_factory=list)
+    provenance: dict = field(default_factory=dict)
 
 
 def decode_loop(load, cfg, policy, tau=None, trigger_mode="joint", dim=None):
@@ -436,5 +438,7 @@ def decode_loop(load, cfg, policy, tau=None, trigger_mode="joint", dim=None):
             selection_ops=int(ops),
             attention_ops=B * 2 * len(pages) * B * dim,
             working_set=list(pages),
+            semantic=[int(i) for i in semantic],
+            provenance=dict(prov),
         ))
     return steps, fired_pages

@@ -52,7 +52,13 @@ __device__ void page_trigger(const ChessState& st, const ChessTriggerCfg& cfg, i
     st.page_stats[2 * s + 1] = var;
     const int g = st.gen_pages[s];
     switch (cfg.policy) {
-      case CHESS_POLICY_NEVER: fire = 0; break;
+      case CHESS_POLICY_NEVER:
+        // no selection ever runs: the semantic set is every sealed page
+        // (simulate.py:179-180), read from the arange the initial selection
+        // stored; the next page-open rebuilds the working set with it
+        fire = 0;
+        st.n_semantic[s] = st.num_sealed[s] + 1;
+        break;
       case CHESS_POLICY_ALWAYS: fire = 1; break;
       case CHESS_POLICY_FIXED: fire = ((g + 1) % cfg.interval) == 0; break;
       case CHESS_POLICY_DYNAMIC: {

@@ -215,12 +215,27 @@ class ChessDecoder:
             _lib.stream_ptr(stream),
         )
 
+    def record_entropy(self, entropies, stream=None):
+        """K5b: per-slot f64 entropies (computed by the caller from its
+        probabilities, simulate.py:160-161) into the open pages' entropy
+        rings; page statistics, trigger and policy at seal as with logits."""
+        _lib.call("chess_record_entropy", self.state.ref, _lib.ptr(entropies), None,
+                  C.byref(self.trig_cfg), _lib.stream_ptr(stream))
+
+    def _uncertainty(self, logits, entropies, entropy_out, stream):
+        if entropies is not None:
+            self.record_entropy(entropies, stream)
+        else:
+            self.entropy_trigger(logits, entropy_out, stream)
+
     def seal(self, stream=None):
         _lib.call("chess_summary_seal", self.state.ref, _lib.stream_ptr(stream))
 
-    def step(self, k_new, v_new, q, logits, out, lse=None, entropy_out=None, stream=None):
+    def step(self, k_new, v_new, q, logits, out, lse=None, entropy_out=None, stream=None, entropies=None):
         """k_new/v_new [b, D] bf16; q/out [b, L, H_q, d] bf16; logits [b, V] f32;
-        lse (optional) f32 [L, b, H_q].
+        lse (optional) f32 [L, b, H_q].  entropies (optional, f64 [b]): the
+        token's entropies when the caller holds probabilities instead of
+        logits (logits is then ignored, chess_record_entropy).
 
         Head shard (self.exchange set): D, H_q are this rank's; `out` is the
         per-layer gather buffer [L, world, b, H_q, d] — K4 writes the rank's
@@ -230,7 +245,7 @@ class ChessDecoder:
         x = self.exchange
         self.append(k_new, v_new, stream)
         if self.concurrent_select and self.kind != "never":
-            self._step_concurrent(q, logits, out, lse, entropy_out, stream)
+            self._step_concurrent(q, logits, out, lse, entropy_out, stream, entropies)
             return
         if x is not None and getattr(x, "fused_outputs", False):
             # outputs gathered by K4's peer stores; one publish/wait/copy per step
@@ -247,12 +262,12 @@ class ChessDecoder:
                 if x is not None:
                     with _on(stream):
                         x.outputs(out[layer])
-        self.entropy_trigger(logits, entropy_out, stream)
+        self._uncertainty(logits, entropies, entropy_out, stream)
         self.seal(stream)
         if self.kind != "never":
             self.select(force_all=False, stream=stream)
 
-    def _step_concurrent(self, q, logits, out, lse, entropy_out, stream):
+    def _step_concurrent(self, q, logits, out, lse, entropy_out, stream, entropies=None):
         """fork { side: entropy+trigger -> seal -> selection (working sets
         deferred) || main: L x decode }, join, flush the pending working sets.
         Same results as the sequential order: the decode reads only KV, q and
@@ -263,7 +278,7 @@ class ChessDecoder:
         fork.record(cur)
         side = self._side
         side.wait_event(fork)
-        self.entropy_trigger(logits, entropy_out, side)
+        self._uncertainty(logits, entropies, entropy_out, side)
         self.seal(side)
         self.select(force_all=False, stream=side, defer_ws=True)
         for layer in range(self.state.shape.layers):
@@ -275,14 +290,14 @@ class ChessDecoder:
         _lib.call("chess_flush_working_sets", self.state.ref, _lib.stream_ptr(cur))
 
     # ------------------------------------------------------------------
-    def capture(self, k_new, v_new, q, logits, out, lse=None, entropy_out=None):
+    def capture(self, k_new, v_new, q, logits, out, lse=None, entropy_out=None, entropies=None):
         """Capture `step` on static buffers as one CUDA graph."""
         g = torch.cuda.CUDAGraph()
         s = torch.cuda.Stream()
         s.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(s):
             with torch.cuda.graph(g, stream=s):
-                self.step(k_new, v_new, q, logits, out, lse, entropy_out, stream=s)
+                self.step(k_new, v_new, q, logits, out, lse, entropy_out, stream=s, entropies=entropies)
         torch.cuda.current_stream().wait_stream(s)
         self.graph = g
         return g

@@ -2,6 +2,14 @@ import os
 import sys
 from pathlib import Path
 
+# Load every kernel of a module when it is registered, not at its first launch.
+# The in-process multi-rank tests run several ranks' streams on one GPU with
+# spinning peer waits (score pulls, the output-gather barrier); a kernel's
+# lazy first-launch load can stall behind such a spinning kernel of another
+# rank until the 10 s wait limit fires.  Must be set before CUDA initialises;
+# spawned rank processes inherit it.
+os.environ.setdefault("CUDA_MODULE_LOADING", "EAGER")
+
 import pytest
 
 REPO = Path(__file__).resolve().parent.parent

@@ -23,6 +23,10 @@ Files
                    (uncertainty.py:22-98) on seeded distributions
   decode_loop.json run_decode_loop under every policy with the working set of
                    every generated page recorded (simulate.py:110-217)
+  acceptance.json  release criteria C1-C3 (pkg/tests/test_acceptance.py:45-112)
+                   and the CPU demo run of BASELINE configs[0] (seed 0, dim
+                   1024, 256 pages of 16, policy always): prefill snapshot
+                   checksums, working sets, budgets, recall
 """
 
 from __future__ import annotations
@@ -262,12 +266,110 @@ def make_decode_loop(pagesel):
     (OUT / "decode_loop.json").write_text(json.dumps(runs))
 
 
+def make_acceptance(pagesel):
+    """Reference outputs of the release criteria the device must reproduce
+    (pkg/tests/test_acceptance.py:45-112) and of the CPU demo run that is
+    BASELINE configs[0].  Inputs are re-drawn by the tests
+    with the same NumPy RNG calls, so only outputs are stored."""
+    from pagesel import (HierarchyIndex, PagedKvStore, QueryAnchor, SelectionConfig, SequenceState,
+                         hierarchical_prune, oracle_flat_topk, reconstruct_working_set, score_all)
+    from pagesel.workload import generate_workload
+
+    doc = {}
+    # C1 (test_acceptance.py:45-65): budgets on 2048 pages, dim 32, seed 0
+    rng = np.random.default_rng(0)
+    index = HierarchyIndex.from_page_vectors(rng.standard_normal((2048, 32)), 8, 8)
+    anchor = QueryAnchor(v=rng.standard_normal(32), source_pages=[])
+    scores = score_all(anchor, *index.coalesced_matrix())
+    doc["c1"] = {}
+    for name in ("aggressive", "moderate", "conservative"):
+        sel = hierarchical_prune(*scores, index.page_to_chunk, index.chunk_to_grid, pagesel.preset_config(name))
+        doc["c1"][name] = [int(i) for i in sel]
+    # C2 (test_acceptance.py:68-86): 200 flat-equivalence instances, seed 1
+    rng = np.random.default_rng(1)
+    c2 = []
+    for _ in range(200):
+        n_pages = int(rng.integers(1, 513))
+        dim = int(rng.integers(8, 257))
+        rho_p = float(rng.uniform(0.05, 1.0))
+        index = HierarchyIndex.from_page_vectors(rng.standard_normal((n_pages, dim)), 4, 4)
+        config = SelectionConfig(pages_per_chunk=4, chunks_per_grid=4, rho_grid=1.0, rho_chunk=1.0, rho_page=rho_p)
+        anchor = QueryAnchor(v=rng.standard_normal(dim), source_pages=[])
+        sc = score_all(anchor, *index.coalesced_matrix())
+        hier = hierarchical_prune(*sc, index.page_to_chunk, index.chunk_to_grid, config)
+        flat = oracle_flat_topk(anchor, index.page_vectors, math.ceil(rho_p * n_pages))
+        assert np.array_equal(hier, flat)
+        c2.append([int(i) for i in hier])
+    doc["c2"] = c2
+    # C3 (test_acceptance.py:89-112): 1000 working-set fuzz cases, seed 2
+    rng = np.random.default_rng(2)
+    c3 = []
+    for trial in range(1000):
+        n_pages = int(rng.integers(1, 128))
+        sinks = int(rng.integers(0, 5))
+        window = int(rng.integers(1, 9))
+        config = SelectionConfig(window_pages=window, sink_pages=sinks)
+        mode = trial % 3
+        if mode == 0:
+            scores = np.zeros(n_pages)
+        elif mode == 1:
+            scores = -np.abs(rng.standard_normal(n_pages))
+        else:
+            scores = rng.standard_normal(n_pages)
+        k = int(rng.integers(0, n_pages + 1))
+        selected = np.sort(np.argsort(-scores, kind="stable")[:k])
+        ws = reconstruct_working_set(selected, SequenceState(page_table=list(range(n_pages)), sink_count=sinks),
+                                     config)
+        c3.append({"selected": [int(i) for i in selected], "pages": [int(i) for i in ws.pages],
+                   "prov": [ws.provenance[p] for p in ws.pages]})
+    doc["c3"] = c3
+    # BASELINE configs[0] / SURVEY §8c: the CPU demo run
+    spec = pagesel.WorkloadSpec(seed=0, dim=1024, context_pages=256, page_size=16, generation_pages=2)
+    cfg = pagesel.preset_config("aggressive", page_size=16)
+    wl = generate_workload(spec)
+    store = PagedKvStore(spec.context_pages + spec.generation_pages + 1, spec.dim, page_size=16)
+    seq = store.create_sequence(cfg)
+    index = HierarchyIndex(spec.dim, cfg.pages_per_chunk, cfg.chunks_per_grid)
+    for t in range(wl.context_keys.shape[0]):
+        ev = store.append_token(seq, wl.context_keys[t], wl.context_values[t])
+        if ev.sealed:
+            index.finalize_page(store.page(ev.page_id), ev.logical_index)
+    snap = index.snapshot()
+    from pagesel import simulate
+
+    recorded = []
+    orig = simulate.reconstruct_working_set
+
+    def rec(selected, seq, config, _orig=orig):
+        ws = _orig(selected, seq, config)
+        recorded.append(list(map(int, ws.pages)))
+        return ws
+
+    simulate.reconstruct_working_set = rec
+    try:
+        rep = pagesel.run_decode_loop(spec, cfg, "always")
+    finally:
+        simulate.reconstruct_working_set = orig
+    doc["cfg1"] = {
+        "spec": {"seed": 0, "dim": 1024, "context_pages": 256, "page_size": 16, "generation_pages": 2},
+        "policy": "always",
+        "prefill_snapshot": snap,
+        "working_sets": recorded,
+        "ws_size": [s.working_set_size for s in rep.steps],
+        "budget_semantic": [s.budget_fraction_semantic for s in rep.steps],
+        "recall": [s.recall for s in rep.steps],
+        "summary": rep.summary(),
+    }
+    (OUT / "acceptance.json").write_text(json.dumps(doc))
+
+
 def main():
     pagesel = _import_reference()
     make_hierarchy(pagesel)
     make_selection(pagesel)
     make_uncertainty(pagesel)
     make_decode_loop(pagesel)
+    make_acceptance(pagesel)
     for f in sorted(OUT.iterdir()):
         if f.suffix in (".npz", ".json"):
             print(f"{f.name}: {f.stat().st_size} bytes")

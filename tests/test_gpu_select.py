@@ -253,3 +253,41 @@ def test_select_model_dimension_streaming_path():
     np.testing.assert_array_equal(sem, _oracle_on(h, cfg, mats)[0])
     np.testing.assert_array_equal(sem, _oracle_on(h, cfg)[0])
     assert set(range(640, 660)) <= set(sem.tolist())  # the planted pages are found
+
+
+def test_select_at_bench_cfg3_state():
+    """The bench's own headline state: cfg3 (Llama-3-8B shape, D = 32768,
+    P = 4096 context pages of 32, batch 16, planted relevance) built by K1b
+    from the KV pool, then one selection pass.  Every slot's selection equals
+    the oracle cascade (selection.py:91-111) run on f64 scores of the
+    device's own f32 mirror rows computed independently (torch f64 GEMV)."""
+    from paper_2602_20732_b200.engine import ChessDecoder
+    from paper_2602_20732_b200.synthetic import SyntheticDecode
+
+    wl = SyntheticDecode("cfg3", batch=16, gen_pages=4, ring=2, kv_budget_gib=8)
+    st, sh = wl.st, wl.shape
+    cfg = preset_config("aggressive", page_size=sh.page_size)
+    dec = ChessDecoder(st, cfg, policy="every_step")
+    wl.prefill(dec)  # K1b build + the post-prefill selection (simulate.py:147-151)
+    P, D = wl.P, sh.dim
+    C = math.ceil(P / 8)
+    G = math.ceil(C / 8)
+    p2c, c2g = np.arange(P) // 8, np.arange(C) // 8
+    for s in range(16):
+        a = st.page_vec64[s, P - cfg.window_pages:P, :D].mean(dim=0)
+        # the anchor the kernels use is the f64 window mean (selection.py:44-59)
+        assert torch.equal(st.anchor[s, :D], a) or torch.allclose(st.anchor[s, :D], a, rtol=1e-15, atol=0)
+        sc = [torch.mv(m[s, :n, :D].double(), st.anchor[s, :D]).cpu().numpy()
+              for m, n in ((st.grid_vec32, G), (st.chunk_vec32, C), (st.page_vec32, P))]
+        sel, info = ref.prune(sc[0], sc[1], sc[2], p2c, c2g, cfg.ratios)
+        sem = st.semantic[s, : int(st.n_semantic[s])].cpu().numpy()
+        np.testing.assert_array_equal(sem, sel, err_msg=f"slot {s}")
+        stats = st.sel_stats[s].cpu().numpy()
+        assert tuple(stats[:5]) == (G, C, P, info["active_c"], info["active_p"])
+        pages, _ = ref.working_set(sel, P, cfg.window_pages, 1)
+        ws = st.ws_logical[s, : int(st.ws_len[s])].cpu().numpy()
+        np.testing.assert_array_equal(ws, pages)
+        np.testing.assert_array_equal(st.block_table[s, : len(pages)].cpu().numpy(),
+                                      wl.table_cpu[s, pages].numpy())
+    del wl, st, dec
+    torch.cuda.empty_cache()

@@ -15,7 +15,7 @@ import pytest
 
 from oracle import attention as attn_ref
 from oracle import pagesel_ref as ref
-from paper_2602_20732_b200.config import SelectionConfig
+from paper_2602_20732_b200.config import PRESETS, SelectionConfig
 
 GOLD = Path(__file__).resolve().parent / "golden"
 
@@ -225,3 +225,82 @@ def test_attention_bf16_bound_covers_kernel_rounding():
                 assert np.all(err <= tol[0, qh]), (trial, (err / tol[0, qh]).max())
                 worst = max(worst, float((err / tol[0, qh]).max()))
     assert worst > 0.05  # the bound is not vacuous
+
+
+# ------------------------------------------------------ acceptance criteria + cfg1 demo run
+def _acceptance():
+    return json.loads((GOLD / "acceptance.json").read_text())
+
+
+def c2_instances():
+    """Inputs of test_acceptance.py:68-86, re-drawn with the same RNG calls."""
+    rng = np.random.default_rng(1)
+    for _ in range(200):
+        n_pages = int(rng.integers(1, 513))
+        dim = int(rng.integers(8, 257))
+        rho_p = float(rng.uniform(0.05, 1.0))
+        rows = rng.standard_normal((n_pages, dim))
+        a = rng.standard_normal(dim)
+        yield rows, a, rho_p
+
+
+def c3_instances():
+    """Inputs of test_acceptance.py:89-112 (sinks, window, scores, k)."""
+    rng = np.random.default_rng(2)
+    for trial in range(1000):
+        n_pages = int(rng.integers(1, 128))
+        sinks = int(rng.integers(0, 5))
+        window = int(rng.integers(1, 9))
+        mode = trial % 3
+        if mode == 0:
+            scores = np.zeros(n_pages)
+        elif mode == 1:
+            scores = -np.abs(rng.standard_normal(n_pages))
+        else:
+            scores = rng.standard_normal(n_pages)
+        k = int(rng.integers(0, n_pages + 1))
+        yield n_pages, sinks, window, scores, k
+
+
+def test_acceptance_c1_c2_c3_oracle():
+    doc = _acceptance()
+    rng = np.random.default_rng(0)
+    h = ref.Hierarchy.from_rows(rng.standard_normal((2048, 32)), 8, 8)
+    a = rng.standard_normal(32)
+    v_all, (g, c, p) = h.coalesced()
+    s = v_all @ a
+    p2c, c2g = h.parent_maps()
+    for name in ("aggressive", "moderate", "conservative"):
+        sel, _ = ref.prune(s[:g], s[g:g + c], s[g + c:], p2c, c2g, PRESETS[name])
+        assert sel.tolist() == doc["c1"][name], name
+    for (rows, a, rho_p), want in zip(c2_instances(), doc["c2"]):
+        h = ref.Hierarchy.from_rows(rows, 4, 4)
+        v_all, (g, c, p) = h.coalesced()
+        s = v_all @ a
+        p2c, c2g = h.parent_maps()
+        hier, _ = ref.prune(s[:g], s[g:g + c], s[g + c:], p2c, c2g, (1.0, 1.0, rho_p))
+        flat = ref.flat_topk(a, h.page_vectors, int(np.ceil(rho_p * rows.shape[0])))
+        assert hier.tolist() == want == flat.tolist()
+    for (n, sinks, window, scores, k), want in zip(c3_instances(), doc["c3"]):
+        sel = np.sort(ref.top_k(scores, k))
+        assert sel.tolist() == want["selected"]
+        pages, prov = ref.working_set(sel, n, window, sinks)
+        assert pages == want["pages"] and [prov[q] for q in pages] == want["prov"]
+
+
+def test_cfg1_demo_run_oracle():
+    """BASELINE configs[0]: the reference CPU demo (seed 0, dim 1024, 256 pages
+    of 16, policy always) — prefill snapshot checksums, working sets, budgets."""
+    run = _acceptance()["cfg1"]
+    load = ref.workload(**run["spec"])
+    cfg = SelectionConfig(page_size=16)
+    B = 16
+    h = ref.Hierarchy(1024, cfg.pages_per_chunk, cfg.chunks_per_grid)
+    for q in range(run["spec"]["context_pages"]):
+        h.fold_page(load["context_keys"][q * B:(q + 1) * B], q)
+    assert h.snapshot() == run["prefill_snapshot"]
+    steps, _ = ref.decode_loop(load, cfg, ("always", None))
+    assert [s.working_set for s in steps] == run["working_sets"]
+    assert [s.working_set_size for s in steps] == run["ws_size"]
+    assert [s.budget_fraction_semantic for s in steps] == run["budget_semantic"]
+    assert [s.recall for s in steps] == run["recall"]
