@@ -20,6 +20,7 @@ def _shape(**kw):
                 pages_per_chunk=2, chunks_per_grid=2, max_pages=24, window_pages=2,
                 max_ws=24, n_phys=64, summary_dtype="f32")
     base.update(kw)
+    base["max_ws"] = max(base["max_ws"], base["max_pages"])
     return Shape(**base)
 
 
