@@ -153,8 +153,16 @@ def run_gpu(args):
     if shard == "batch" and args.batch is None:
         batch = max(1, c["batch"] // world)
     head = shard == "head"
-    total_steps = args.warmup + args.steps
     ring = 64 if c["page"] == 32 else 32
+    # variants (dynamic, attention-only) run at least two rings so their
+    # per-step time amortises whole pages: seals, and triggers on the
+    # scheduled unstable pages (one page in two)
+    var_steps = max(args.steps, 2 * ring)
+    # pre-roll: W generated pages seal before anything is timed, so the Eq.3
+    # anchor is built from generated pages (which carry the planted signal)
+    # and the semantic sets are the steady-state ones, whatever --steps is
+    pre_roll = 4 * c["page"]
+    total_steps = pre_roll + args.warmup + max(args.steps, var_steps)
     gen_pages = math.ceil((total_steps + 2 * ring + 64) / c["page"]) + 4
     wl = SyntheticDecode(cfg_name, batch=batch, gen_pages=gen_pages, ring=ring, seed=rank,
                          summary_dtype=args.summary_dtype, head_shard=(rank, world) if head else None,
@@ -185,10 +193,11 @@ def run_gpu(args):
         dec = ChessDecoder(st, sel, policy=policy, thresholds=thresholds, full_scan=args.full_scan,
                            exchange=exchange)
         wl.prefill(dec)
-        # one eager step: first-call attribute/occupancy setup (and the NCCL
-        # communicator) happen outside capture
-        k, v, q, lg = wl.step_inputs(ring - 1)
-        dec.step(k, v, q, lg, outs[0])
+        # eager pre-roll (first-call attribute/occupancy setup and the NCCL
+        # communicator happen outside capture): W generated pages seal
+        for t in range(pre_roll):
+            k, v, q, lg = wl.step_inputs(t)
+            dec.step(k, v, q, lg, outs[0])
         torch.cuda.synchronize()
         return dec
 
@@ -201,9 +210,11 @@ def run_gpu(args):
         outs = [wl.out, torch.zeros_like(wl.out)]
 
     def capture_ring(dec):
+        # graph i replays ring input (pre_roll + i) % ring: the token stream
+        # continues where the pre-roll stopped
         graphs = []
         for r in range(ring):
-            k, v, q, lg = wl.step_inputs(r)
+            k, v, q, lg = wl.step_inputs(pre_roll + r)
             graphs.append(dec.capture(k, v, q, lg, outs[r % 2]))
         return graphs
 
@@ -218,7 +229,8 @@ def run_gpu(args):
         t1 = torch.cuda.Event(enable_timing=True)
         sampler = ClockSampler(local) if sample_clocks else None
         ws_before = st.ws_len.float().mean().item()
-        stats_before = st.sel_stats.clone()
+        trig0 = int(st.trigger_count.sum().item())
+        sealed0 = int(st.gen_pages.sum().item())
         fill0 = int(st.tail_fill[0].item())
         torch.cuda.synchronize()
         if sampler:
@@ -244,7 +256,8 @@ def run_gpu(args):
             "ws_mean": 0.5 * (ws_before + ws_after),
             "mean_fill": float(np.mean(fills)),
             "sel_stats": st.sel_stats.cpu().numpy(),
-            "triggers": int(st.gen_pages.sum().item()),
+            "pages_sealed": int(st.gen_pages.sum().item()) - sealed0,
+            "triggers": int(st.trigger_count.sum().item()) - trig0,
             "clocks": sampler.summary() if sampler else None,
         }
 
@@ -276,7 +289,7 @@ def run_gpu(args):
 
     # ---- kernel-level timing: the kernels alone, captured in CUDA graphs
     # (no host gaps) and timed with CUDA events on the replay stream ----
-    k, v, q, lg = wl.step_inputs(0)
+    k, v, q, lg = wl.step_inputs(pre_roll + args.warmup + args.steps)
     reps = 3
     gs = torch.cuda.Stream()
     gs.wait_stream(torch.cuda.current_stream())
@@ -305,6 +318,14 @@ def run_gpu(args):
     del g_attn, g_sel
     ws_now = st.ws_len.float().mean().item()
     fill_now = float(st.tail_fill.float().mean().item())
+    # (page, kv-head) tiles one K4 launch streams, and how many are distinct
+    # physical tiles (a page shared by two slots' working sets would be an
+    # L2 hit inside the launch)
+    wl_now = st.ws_len.cpu().numpy()
+    bt_now = st.block_table.cpu().numpy()
+    phys_now = np.concatenate([bt_now[s_, : wl_now[s_]] for s_ in range(batch)])
+    k4_tiles = int(phys_now.size) * sh.kv_heads
+    k4_unique_tiles = int(np.unique(phys_now).size) * sh.kv_heads
     attn_launch_bytes = attn_bytes_per_layer(ws_now, fill_now)
     sel_call_bytes = select_bytes(st.sel_stats.cpu().numpy())
 
@@ -312,7 +333,10 @@ def run_gpu(args):
     # headline variant.  Every step's inputs are copied host->device and its
     # attention output device->host inside the timed region; the copies run
     # on their own streams, pipelined one step ahead/behind the compute. ----
-    hk = [t.cpu().pin_memory() for t in (wl.k_ring[0], wl.v_ring[0], wl.q_ring[0], wl.logit_ring[0])]
+    # every ring slot's own inputs on the host (pinned): each step copies its
+    # token's K/V rows, q and logits (and the device ring keeps the right
+    # inputs for the variants timed afterwards)
+    hk = [t.cpu().pin_memory() for t in (wl.k_ring, wl.v_ring, wl.q_ring, wl.logit_ring)]
     h_out = [torch.empty(outs[0].shape, dtype=outs[0].dtype).pin_memory() for _ in range(2)]
     dec = fresh_decoder("every_step")
     graphs = capture_ring(dec)
@@ -328,11 +352,13 @@ def run_gpu(args):
     d2h_ev = [torch.cuda.Event() for _ in range(2)]
 
     def h2d(r):
+        # the input slot graph r reads (capture_ring)
+        slot = (pre_roll + r) % ring
         with torch.cuda.stream(cs):
-            wl.k_ring[r].copy_(hk[0], non_blocking=True)
-            wl.v_ring[r].copy_(hk[1], non_blocking=True)
-            wl.q_ring[r].copy_(hk[2], non_blocking=True)
-            wl.logit_ring[r].copy_(hk[3], non_blocking=True)
+            wl.k_ring[slot].copy_(hk[0][slot], non_blocking=True)
+            wl.v_ring[slot].copy_(hk[1][slot], non_blocking=True)
+            wl.q_ring[slot].copy_(hk[2][slot], non_blocking=True)
+            wl.logit_ring[slot].copy_(hk[3][slot], non_blocking=True)
             h2d_ev[r].record(cs)
 
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -362,17 +388,17 @@ def run_gpu(args):
         tt = torch.tensor([e2e_ms], device="cuda")
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         e2e_ms = tt.item()
-    h2d = sum(t.numel() * t.element_size() for t in hk)
+    h2d = sum(t[0].numel() * t.element_size() for t in hk)
     d2h = h_out[0].numel() * h_out[0].element_size()
 
     # ---- amortised dynamic (backtracking) and attention-only variants ----
     if not args.headline_only:
         dec = fresh_decoder("dynamic", wl.tau)
         graphs = capture_ring(dec)
-        results["dynamic"] = timed(dec, graphs, args.steps, args.warmup)
+        results["dynamic"] = timed(dec, graphs, var_steps, args.warmup)
         dec = fresh_decoder("fixed(1000000)")
         graphs = capture_ring(dec)
-        results["attn_only"] = timed(dec, graphs, args.steps, args.warmup)
+        results["attn_only"] = timed(dec, graphs, var_steps, args.warmup)
     del graphs
 
     head = results["select_every_step"]
@@ -414,6 +440,8 @@ def run_gpu(args):
             "kv_aliased": wl.aliased,
             "l2": "inputs larger than L2 (step reads >> 126 MB)",
             "ws_pages_mean": head["ws_mean"],
+            "pre_roll_tokens": pre_roll,
+            "generated_pages_sealed_before_timing": 4,
         },
         "bytes_per_step": bytes_step,
         "step_roofline": {"achieved": bytes_step / (ms_step / 1e3) / 1e9, "peak": hbm_peak, "unit": "GB/s",
@@ -429,6 +457,8 @@ def run_gpu(args):
             "traffic": _ncu_traffic(cfg_name, "sparse_decode"),
             "bytes_per_launch": attn_launch_bytes,
             "launch_us": attn_launch_s * 1e6,
+            "tiles_per_launch": k4_tiles,
+            "unique_tiles_per_launch": k4_unique_tiles,
         },
         "select_roofline": {
             "kernel": "select cascade (K2+K3, 3 launches)",
@@ -449,13 +479,16 @@ def run_gpu(args):
         "clocks": head["clocks"],
     }
     if not args.headline_only:
+        nsteps = {"select_every_step": args.steps, "dynamic": var_steps, "attn_only": var_steps}
         out["variants"] = {
-            name: {"us_per_step": r["ms"] / args.steps * 1e3,
-                   "tokens_per_s": job_batch / (r["ms"] / args.steps / 1e3),
-                   "ws_pages_mean": r["ws_mean"]}
+            name: {"us_per_step": r["ms"] / nsteps[name] * 1e3,
+                   "tokens_per_s": job_batch / (r["ms"] / nsteps[name] / 1e3),
+                   "steps": nsteps[name],
+                   "ws_pages_mean": r["ws_mean"],
+                   "generated_pages_sealed": r["pages_sealed"],
+                   "triggers_fired": r["triggers"]}
             for name, r in results.items()
         }
-        out["variants"]["dynamic"]["generated_pages_sealed"] = results["dynamic"]["triggers"]
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(cfg_name, steps=1)
     if rank == 0:
@@ -571,9 +604,47 @@ def run_reference(args):
     }), flush=True)
 
 
+def _spawn_ranks(n):
+    """`bench.py --gpus N` outside torchrun: launch N ranks of this same
+    command (one process per GPU) the way the driver does, and return the
+    launcher's exit code.  Rank 0 prints the JSON line."""
+    import socket
+    import subprocess
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", str(Path(__file__).resolve()), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
+def run_plumbing(args):
+    """CHESS_BENCH_PLUMBING=1 (tests only, no GPU): the multi-rank skeleton
+    of run_gpu — process group, barrier, max-over-ranks timing, rank-0
+    output — over gloo, without touching a device."""
+    import torch.distributed as dist
+
+    rank, world, _ = _dist_env()
+    if world > 1:
+        dist.init_process_group("gloo")
+    t = torch.tensor([float(rank + 1)])
+    ranks = [torch.zeros(1) for _ in range(world)]
+    if world > 1:
+        dist.barrier()
+        dist.all_gather(ranks, torch.tensor([float(rank)]))
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    if rank == 0:
+        print(json.dumps({"plumbing": True, "n_gpus": world, "ranks": [int(r.item()) for r in ranks],
+                          "max_over_ranks": t.item()}), flush=True)
+    if dist.is_initialized():
+        dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--gpus", type=int, default=None,
+                    help="GPUs (ranks) of the job; outside torchrun, N > 1 launches N ranks itself")
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="chess", choices=["chess", "reference"])
@@ -593,6 +664,18 @@ def main():
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    env_world = os.environ.get("WORLD_SIZE")
+    if env_world is None and args.gpus is not None and args.gpus > 1:
+        sys.exit(_spawn_ranks(args.gpus))
+    world = int(env_world) if env_world is not None else 1
+    if args.gpus is not None and args.gpus != world:
+        sys.exit(f"bench.py: --gpus {args.gpus} but the launcher started {world} rank(s)")
+    if os.environ.get("CHESS_BENCH_PLUMBING") == "1":
+        run_plumbing(args)
+        return
+    if (args.impl != "reference" and os.environ.get("CHESS_BENCH_ONE_DEVICE") != "1"
+            and torch.cuda.device_count() < world):
+        sys.exit(f"bench.py: {world} ranks but only {torch.cuda.device_count()} visible GPU(s)")
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -135,6 +135,8 @@ typedef struct ChessState {
   int32_t* gen_pages;    /* [batch] generated pages completed                    */
   double* page_stats;    /* [batch][2] (mean_entropy, varentropy) of last page   */
   uint8_t* fire;         /* [batch] selection gate                               */
+  uint32_t* trigger_count; /* [batch] sealed pages whose policy decision fired a
+                          * reselection (backtracking events); may be NULL     */
   /* Optional device page pool: PagedKvStore's free list (kv_store.py:103-136)
    * on the device, so generation never returns to the host for a page.
    * pool_free == NULL: the caller fills page_table (host-managed).  A slot's

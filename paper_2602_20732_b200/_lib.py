@@ -59,7 +59,7 @@ STATE_POINTERS = [
     "sink_count", "sealed", "num_sealed", "page_vec64", "chunk_sum64", "grid_sum64",
     "chunk_vec64", "grid_vec64", "page_vec32", "chunk_vec32", "grid_vec32", "key_sum",
     "anchor", "semantic", "n_semantic", "sel_stats", "ws_logical", "block_table",
-    "ws_prov", "ws_len", "ent_ring", "ent_count", "gen_pages", "page_stats", "fire",
+    "ws_prov", "ws_len", "ent_ring", "ent_count", "gen_pages", "page_stats", "fire", "trigger_count",
     "pool_free", "pool_top", "pool_base", "pool_end", "pool_oom",
     "workspace",
 ]

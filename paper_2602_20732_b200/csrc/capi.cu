@@ -9,6 +9,19 @@
 #include <mutex>
 
 #include "common.cuh"
+#include <nvtx3/nvToolsExt.h>
+
+// One NVTX range per C-ABI call (SURVEY.md §5 "Tracing / profiling"): host-side
+// push/pop around the launch, so an nsys timeline names each kernel's entry
+// point.  Header-only NVTX v3: without an attached tool a push is one
+// predicted-not-taken branch.
+namespace {
+struct NvtxScope {
+  explicit NvtxScope(const char* name) { nvtxRangePushA(name); }
+  ~NvtxScope() { nvtxRangePop(); }
+};
+}  // namespace
+#define CHESS_NVTX(name) NvtxScope chess_nvtx_scope_(name)
 
 namespace chess {
 
@@ -217,6 +230,7 @@ size_t chess_workspace_bytes(const ChessDims* d) {
 }
 
 int chess_reset_slots(const ChessState* st, const uint8_t* mask, void* stream) {
+  CHESS_NVTX("chess_reset_slots");
   Workspace ws;
   int rc = state_ws(st, &ws);
   if (rc) return rc;
@@ -225,6 +239,7 @@ int chess_reset_slots(const ChessState* st, const uint8_t* mask, void* stream) {
 
 int chess_append_kv(const ChessState* st, const void* k_rows, const void* v_rows,
                     int64_t row_stride, const uint8_t* active, void* stream) {
+  CHESS_NVTX("chess_append_kv");
   Workspace ws;
   int rc = state_ws(st, &ws);
   if (rc) return rc;
@@ -234,6 +249,7 @@ int chess_append_kv(const ChessState* st, const void* k_rows, const void* v_rows
 
 int chess_append_kv_layers(const ChessState* st, int32_t layer_begin, int32_t layer_end, const void* k_rows,
                            const void* v_rows, int64_t row_stride, const uint8_t* active, void* stream) {
+  CHESS_NVTX("chess_append_kv_layers");
   Workspace ws;
   int rc = state_ws(st, &ws);
   if (rc) return rc;
@@ -249,6 +265,7 @@ int chess_append_kv_layers(const ChessState* st, int32_t layer_begin, int32_t la
 }
 
 int chess_summary_seal(const ChessState* st, void* stream) {
+  CHESS_NVTX("chess_summary_seal");
   Workspace ws;
   int rc = state_ws(st, &ws);
   if (rc) return rc;
@@ -256,6 +273,7 @@ int chess_summary_seal(const ChessState* st, void* stream) {
 }
 
 int chess_summary_build(const ChessState* st, const int32_t* n_pages, void* stream) {
+  CHESS_NVTX("chess_summary_build");
   Workspace ws;
   int rc = state_ws(st, &ws);
   if (rc) return rc;
@@ -265,6 +283,7 @@ int chess_summary_build(const ChessState* st, const int32_t* n_pages, void* stre
 
 int chess_summary_from_vectors(const ChessState* st, int32_t seq, const double* rows, int32_t n,
                                int64_t row_stride, void* stream) {
+  CHESS_NVTX("chess_summary_from_vectors");
   Workspace ws;
   int rc = state_ws(st, &ws);
   if (rc) return rc;
@@ -280,6 +299,7 @@ int chess_summary_from_vectors(const ChessState* st, int32_t seq, const double* 
 
 int chess_summary_fold(const ChessState* st, int32_t seq, const void* rows, int32_t dtype,
                        int32_t n_rows, int64_t row_stride, void* stream) {
+  CHESS_NVTX("chess_summary_fold");
   Workspace ws;
   int rc = state_ws(st, &ws);
   if (rc) return rc;
@@ -292,6 +312,7 @@ int chess_summary_fold(const ChessState* st, int32_t seq, const void* rows, int3
 
 int chess_record_entropy(const ChessState* st, const double* entropy, const uint8_t* active,
                          const ChessTriggerCfg* cfg, void* stream) {
+  CHESS_NVTX("chess_record_entropy");
   Workspace ws;
   int rc = state_ws(st, &ws);
   if (rc) return rc;
@@ -321,6 +342,7 @@ static int select_params(const ChessSelectCfg* cfg, SelParams* out) {
 }
 
 int chess_select(const ChessState* st, const ChessSelectCfg* cfg, void* stream) {
+  CHESS_NVTX("chess_select");
   Workspace ws;
   int rc = state_ws(st, &ws);
   if (rc) return rc;
@@ -347,6 +369,7 @@ static int check_level(const ChessState* st, const ChessSelectCfg* cfg, int32_t 
 
 int chess_select_partial(const ChessState* st, const ChessSelectCfg* cfg, int32_t level,
                          double* partial, int64_t ld_partial, void* stream) {
+  CHESS_NVTX("chess_select_partial");
   Workspace ws;
   int rc = state_ws(st, &ws);
   if (rc) return rc;
@@ -361,6 +384,7 @@ int chess_select_partial(const ChessState* st, const ChessSelectCfg* cfg, int32_
 
 int chess_select_combine(const ChessState* st, const ChessSelectCfg* cfg, int32_t level,
                          const double* gathered, int32_t world, int64_t ld_partial, void* stream) {
+  CHESS_NVTX("chess_select_combine");
   Workspace ws;
   int rc = state_ws(st, &ws);
   if (rc) return rc;
@@ -394,6 +418,7 @@ static int peer_params(const ChessState* st, const ChessSelectCfg* cfg, int32_t 
 
 int chess_select_push(const ChessState* st, const ChessSelectCfg* cfg, int32_t level,
                       const ChessPeerExchange* px, void* stream) {
+  CHESS_NVTX("chess_select_push");
   Workspace ws;
   int rc = state_ws(st, &ws);
   if (rc) return rc;
@@ -404,6 +429,7 @@ int chess_select_push(const ChessState* st, const ChessSelectCfg* cfg, int32_t l
 
 int chess_select_pull(const ChessState* st, const ChessSelectCfg* cfg, int32_t level,
                       const ChessPeerExchange* px, void* stream) {
+  CHESS_NVTX("chess_select_pull");
   Workspace ws;
   int rc = state_ws(st, &ws);
   if (rc) return rc;
@@ -450,6 +476,7 @@ static int pool_state(const ChessState* st) {
 }
 
 int chess_pool_init(const ChessState* st, const int32_t* ids, int32_t n, void* stream) {
+  CHESS_NVTX("chess_pool_init");
   int rc = pool_state(st);
   if (rc) return rc;
   if (n < 0 || n > st->d.n_phys) return fail(CHESS_ERR_CONFIG, "pool of %d pages > n_phys %lld", n, (long long)st->d.n_phys);
@@ -458,6 +485,7 @@ int chess_pool_init(const ChessState* st, const int32_t* ids, int32_t n, void* s
 }
 
 int chess_pool_reserve(const ChessState* st, const int32_t* counts, void* stream) {
+  CHESS_NVTX("chess_pool_reserve");
   int rc = pool_state(st);
   if (rc) return rc;
   if (!counts) return fail(CHESS_ERR_SHAPE, "pool_reserve: null counts");
@@ -465,12 +493,14 @@ int chess_pool_reserve(const ChessState* st, const int32_t* counts, void* stream
 }
 
 int chess_pool_release(const ChessState* st, const uint8_t* mask, void* stream) {
+  CHESS_NVTX("chess_pool_release");
   int rc = pool_state(st);
   if (rc) return rc;
   return launch_pool_release(*st, mask, (cudaStream_t)stream);
 }
 
 int chess_flush_working_sets(const ChessState* st, void* stream) {
+  CHESS_NVTX("chess_flush_working_sets");
   Workspace ws;
   int rc = state_ws(st, &ws);
   if (rc) return rc;
@@ -478,6 +508,7 @@ int chess_flush_working_sets(const ChessState* st, void* stream) {
 }
 
 int chess_build_working_set(const ChessState* st, void* stream) {
+  CHESS_NVTX("chess_build_working_set");
   Workspace ws;
   int rc = state_ws(st, &ws);
   if (rc) return rc;
@@ -493,6 +524,7 @@ int chess_sparse_decode(const ChessState* st, int32_t layer, const void* q, int6
 int chess_sparse_decode_ex(const ChessState* st, int32_t layer, const void* q, int64_t q_stride,
                            void* out, int64_t out_stride, float* lse, float softmax_scale,
                            uint32_t flags, void* stream) {
+  CHESS_NVTX("chess_sparse_decode_ex");
   Workspace ws;
   int rc = state_ws(st, &ws);
   if (rc) return rc;
@@ -524,6 +556,7 @@ static int64_t gather_block(const ChessDims& d) { return (int64_t)d.batch * d.q_
 int chess_sparse_decode_gather(const ChessState* st, int32_t layer, const void* q, int64_t q_stride,
                                void* out, int64_t out_stride, float* lse, float softmax_scale,
                                uint32_t flags, const ChessPeerOutputs* po, void* stream) {
+  CHESS_NVTX("chess_sparse_decode_gather");
   Workspace ws;
   int rc = state_ws(st, &ws);
   if (rc) return rc;
@@ -547,6 +580,7 @@ int chess_sparse_decode_gather(const ChessState* st, int32_t layer, const void* 
 }
 
 int chess_gather_finish(const ChessState* st, const ChessPeerOutputs* po, void* out, void* stream) {
+  CHESS_NVTX("chess_gather_finish");
   int rc;
   if ((rc = check_peer_outputs(st, po))) return rc;
   const int64_t elems = (int64_t)st->d.layers * po->world * gather_block(st->d);
@@ -558,6 +592,7 @@ int chess_gather_finish(const ChessState* st, const ChessPeerOutputs* po, void* 
 
 int chess_entropy_trigger(const ChessState* st, const float* logits, int64_t vocab, int64_t ld,
                           const ChessTriggerCfg* cfg, double* entropy_out, void* stream) {
+  CHESS_NVTX("chess_entropy_trigger");
   Workspace ws;
   int rc = state_ws(st, &ws);
   if (rc) return rc;
@@ -570,6 +605,7 @@ int chess_entropy_trigger(const ChessState* st, const float* logits, int64_t voc
 
 int chess_score_rows(const void* rows, int32_t dtype, int64_t n_rows, int64_t dim, int64_t ld,
                      const double* anchor, double* scores, void* stream) {
+  CHESS_NVTX("chess_score_rows");
   if (n_rows < 0 || dim < 0 || ld < dim) return fail(CHESS_ERR_SHAPE, "score_rows: bad shape");
   if (dtype < 0 || dtype > 2) return fail(CHESS_ERR_CONFIG, "bad dtype");
   return launch_score_rows(rows, dtype, n_rows, dim, ld, anchor, scores, (cudaStream_t)stream);
@@ -577,6 +613,7 @@ int chess_score_rows(const void* rows, int32_t dtype, int64_t n_rows, int64_t di
 
 int chess_mean_rows(const void* rows, int32_t dtype, int64_t n_rows, int64_t dim, int64_t ld,
                     double* out, void* stream) {
+  CHESS_NVTX("chess_mean_rows");
   if (n_rows < 1) return fail(CHESS_ERR_EMPTY_CONTEXT, "no rows to average");
   if (dim < 0 || ld < dim) return fail(CHESS_ERR_SHAPE, "mean_rows: bad shape");
   if (dim == 0) return CHESS_OK;
@@ -594,6 +631,7 @@ int chess_prune(const double* s_g, int32_t G, const double* s_c, int32_t C, cons
                 int32_t P, const int64_t* page_to_chunk, const int64_t* chunk_to_grid,
                 double rho_grid, double rho_chunk, double rho_page, int32_t* out_pages,
                 int32_t* out_count, void* workspace, void* stream) {
+  CHESS_NVTX("chess_prune");
   if (G < 0 || C < 0 || P < 0) return fail(CHESS_ERR_SHAPE, "prune: negative sizes");
   return launch_prune(s_g, G, s_c, C, s_p, P, page_to_chunk, chunk_to_grid, rho_grid, rho_chunk,
                       rho_page, out_pages, out_count, workspace, (cudaStream_t)stream);
@@ -602,6 +640,7 @@ int chess_prune(const double* s_g, int32_t G, const double* s_c, int32_t C, cons
 int chess_topk(const double* scores, int32_t n, int32_t k, const uint8_t* active,
                int32_t* out_idx, int32_t* out_count, int32_t sorted, void* workspace,
                void* stream) {
+  CHESS_NVTX("chess_topk");
   if (n < 0) return fail(CHESS_ERR_SHAPE, "topk: negative n");
   return launch_topk(scores, n, k, active, out_idx, out_count, sorted, workspace,
                      (cudaStream_t)stream);
@@ -610,6 +649,7 @@ int chess_topk(const double* scores, int32_t n, int32_t k, const uint8_t* active
 int chess_working_set(const int32_t* selected, int32_t n_sel, int32_t n_pages, int32_t window,
                       int32_t sinks, const int32_t* page_table, int32_t* out_pages,
                       int8_t* out_prov, int32_t* out_phys, int32_t* out_len, void* stream) {
+  CHESS_NVTX("chess_working_set");
   if (window < 1) return fail(CHESS_ERR_CONFIG, "window_pages must be >= 1");
   if (sinks < 0) return fail(CHESS_ERR_CONFIG, "sink_pages must be >= 0");
   if (n_pages < 0 || n_sel < 0) return fail(CHESS_ERR_SHAPE, "working_set: negative sizes");
@@ -619,11 +659,13 @@ int chess_working_set(const int32_t* selected, int32_t n_sel, int32_t n_pages, i
 
 int chess_gather_pages(const int32_t* page_table, int32_t n_pages, const int64_t* idx, int32_t n,
                        int32_t* out, int32_t* err, void* stream) {
+  CHESS_NVTX("chess_gather_pages");
   return launch_gather_pages(page_table, n_pages, idx, n, out, err, (cudaStream_t)stream);
 }
 
 int chess_entropy_probs(const double* probs, int64_t rows, int64_t n, int64_t ld, double* out,
                         int32_t* flags, void* stream) {
+  CHESS_NVTX("chess_entropy_probs");
   if (rows < 0 || n < 1 || ld < n) return fail(CHESS_ERR_SHAPE, "entropy_probs: bad shape");
   return launch_entropy_probs(probs, rows, n, ld, out, flags, (cudaStream_t)stream);
 }
@@ -634,6 +676,7 @@ size_t chess_entropy_workspace_bytes(int64_t rows) {
 
 int chess_entropy_logits(const float* logits, int64_t rows, int64_t vocab, int64_t ld, double* out,
                          void* workspace, void* stream) {
+  CHESS_NVTX("chess_entropy_logits");
   if (rows < 0 || vocab < 1 || ld < vocab) return fail(CHESS_ERR_SHAPE, "entropy_logits: bad shape");
   if (rows == 0) return CHESS_OK;
   Workspace ws{};
@@ -649,6 +692,7 @@ size_t chess_calibrate_workspace_bytes(int32_t n_pages) {
 
 int chess_calibrate(const double* entropies, const int32_t* counts, int32_t n_pages, int64_t ld,
                     double percentile, double* out, void* workspace, void* stream) {
+  CHESS_NVTX("chess_calibrate");
   // CalibrationError cases (uncertainty.py:66-69) -> ValueError status
   if (n_pages < 1) return fail(CHESS_ERR_VALUE, "cannot calibrate on an empty sample");
   if (!(percentile > 0.0 && percentile < 1.0))
@@ -662,6 +706,7 @@ int chess_calibrate(const double* entropies, const int32_t* counts, int32_t n_pa
 }
 
 int chess_page_uncertainty(const double* ent, int32_t n, double* out, void* stream) {
+  CHESS_NVTX("chess_page_uncertainty");
   if (n < 1) return fail(CHESS_ERR_VALUE, "page has no generated tokens");
 
   return launch_page_uncertainty(ent, n, out, (cudaStream_t)stream);

@@ -70,6 +70,7 @@ __device__ void page_trigger(const ChessState& st, const ChessTriggerCfg& cfg, i
       default: fire = 1; break;
     }
     st.gen_pages[s] = g + 1;
+    if (fire && st.trigger_count) st.trigger_count[s] += 1u;
   }
   st.fire[s] = fire;
 }

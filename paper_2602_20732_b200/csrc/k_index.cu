@@ -167,6 +167,7 @@ __global__ void reset_kernel(ChessState st, const uint8_t* mask) {
     st.ent_count[s] = 0;
     st.gen_pages[s] = 0;
     st.fire[s] = 0;
+    if (st.trigger_count) st.trigger_count[s] = 0;
     st.page_stats[2 * s] = 0.0;
     st.page_stats[2 * s + 1] = 0.0;
     for (int i = 0; i < 8; ++i) st.sel_stats[8 * s + i] = 0;

@@ -105,6 +105,7 @@ class DecodeState:
         self.gen_pages = torch.zeros(b, **i32)
         self.page_stats = torch.zeros((b, 2), **f64)
         self.fire = torch.zeros(b, **u8)
+        self.trigger_count = torch.zeros(b, **i32)
         # optional device page pool (kv_store.py:103-136 free list on the device)
         if page_pool:
             self.pool_free = torch.zeros(s.n_phys, **i32)

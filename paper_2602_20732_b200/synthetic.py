@@ -13,10 +13,14 @@ relevance recipe (workload.py:96-137) restated per head slice, on device:
     lambda = 1 - e^-2 on odd tokens (workload.py:116-126).
 
 KV capacity: at full layer count the context KV of cfg3/cfg4/cfg5 exceeds one
-B200's HBM, so logical context pages alias onto a smaller physical pool
-(phys = (slot*P + p) mod n_ctx_phys).  Bytes reported are the logical bytes
-read; the pool stays far larger than L2 (126 MB).  Generated pages get
-dedicated physical pages.
+B200's HBM, so logical context pages alias onto a smaller physical pool.
+Every page a steady-state working set holds — the sink, the planted relevant
+run, the last context pages (window) and every generated page — gets a
+dedicated physical page, so working sets of different slots never share a
+page (no L2 hits between slots inside one attention launch); only the
+remaining background context pages alias, onto the rest of the pool
+(phys = n_dedicated + (slot*P + p) mod n_background).  Bytes reported are the
+logical bytes read; the pool stays far larger than L2 (126 MB).
 """
 
 from __future__ import annotations
@@ -135,21 +139,12 @@ class SyntheticDecode:
         self._make_inputs(ring)
 
     # ------------------------------------------------------------------
+    DEDICATED_TAIL = 8  # last context pages with dedicated physical pages (>= the window)
+
     def _fill_tables(self):
         b, P, B = self.batch, self.P, self.B
         st = self.st
         mp = self.shape.max_pages
-        tab = torch.empty((b, mp), dtype=torch.int64)
-        ar = torch.arange(P, dtype=torch.int64)
-        for s in range(b):
-            tab[s, :P] = (s * P + ar) % self.n_ctx_phys
-            g = mp - P
-            tab[s, P:] = self.n_ctx_phys + s * g + torch.arange(g)
-        st.page_table.copy_(tab.to(torch.int32))
-        st.num_pages.fill_(P)
-        st.tail_fill.fill_(B)
-        st.token_count.fill_(P * B)
-        st.sink_count.fill_(1)
         # planted relevant pages: ceil(1%) clustered, chunk-aligned (workload.py:72-86)
         rng = np.random.default_rng(1234)
         n_rel = max(1, round(0.01 * P))
@@ -159,6 +154,31 @@ class SyntheticDecode:
             n_starts = max(1, (P - n_rel) // nc + 1)
             start = min(int(rng.integers(n_starts)) * nc, P - n_rel)
             self.relevant.append(list(range(start, start + n_rel)))
+        tab = torch.empty((b, mp), dtype=torch.int64)
+        ar = torch.arange(P, dtype=torch.int64)
+        g = mp - P
+        if not self.aliased:
+            for s in range(b):
+                tab[s, :P] = s * P + ar
+        else:
+            ded = [sorted({0, *self.relevant[s], *range(max(0, P - self.DEDICATED_TAIL), P)}) for s in range(b)]
+            n_ded = sum(len(d_) for d_ in ded)
+            n_bg = self.n_ctx_phys - n_ded
+            if n_bg < 1:
+                raise ValueError("KV pool too small for the dedicated working-set pages")
+            nxt = 0
+            for s in range(b):
+                tab[s, :P] = n_ded + (s * P + ar) % n_bg
+                d_ = torch.as_tensor(ded[s], dtype=torch.int64)
+                tab[s, d_] = nxt + torch.arange(len(ded[s]))
+                nxt += len(ded[s])
+        for s in range(b):
+            tab[s, P:] = self.n_ctx_phys + s * g + torch.arange(g)
+        st.page_table.copy_(tab.to(torch.int32))
+        st.num_pages.fill_(P)
+        st.tail_fill.fill_(B)
+        st.token_count.fill_(P * B)
+        st.sink_count.fill_(1)
         self.table_cpu = tab
 
     def _fill_kv(self, seed):
