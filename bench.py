@@ -231,6 +231,7 @@ def run_gpu(args):
         ws_before = st.ws_len.float().mean().item()
         trig0 = int(st.trigger_count.sum().item())
         sealed0 = int(st.gen_pages.sum().item())
+        resc0 = tc_rescored()
         fill0 = int(st.tail_fill[0].item())
         torch.cuda.synchronize()
         if sampler:
@@ -258,6 +259,8 @@ def run_gpu(args):
             "sel_stats": st.sel_stats.cpu().numpy(),
             "pages_sealed": int(st.gen_pages.sum().item()) - sealed0,
             "triggers": int(st.trigger_count.sum().item()) - trig0,
+            "rescored_rows": tc_rescored() - resc0,
+            "steps": steps,
             "clocks": sampler.summary() if sampler else None,
         }
 
@@ -267,17 +270,38 @@ def run_gpu(args):
         qo = batch * sh.q_heads * sh.head_dim * 2 * 2
         return kv + qo
 
-    def select_bytes(stats):
+    def tc_rescored():
+        """f16tc: cumulative rows the exact f64 pass rescored (all slots)."""
+        if args.summary_dtype != "f16tc":
+            return 0
+        import ctypes
+        lib = _lib.load()
+        lib.chess_debug_tc_read.argtypes = [ctypes.c_void_p, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32] + [ctypes.c_void_p] * 5
+        meta = np.zeros(4, np.int32)
+        tot = 0
+        for s_ in range(batch):
+            _lib.check(lib.chess_debug_tc_read(st.ref, s_, 0, 0, None, None, None, meta.ctypes.data, None), "tc_read")
+            tot += int(meta[3])
+        return tot
+
+    def select_bytes(stats, res=None):
         # rows actually scanned: G + A_c + A_p per sequence, f32/f64 rows; + anchor
-        es = {"f32": 4, "f64": 8, "bf16": 2}[args.summary_dtype]
+        es = {"f32": 4, "f64": 8, "bf16": 2, "f16tc": 2}[args.summary_dtype]
         rows = stats[:, 0] + stats[:, 3] + stats[:, 4] if not args.full_scan else stats[:, 0] + stats[:, 1] + stats[:, 2]
-        return float(np.sum(rows) * sh.dim * es + batch * sh.dim * 8)
+        b = float(np.sum(rows) * sh.dim * es + batch * sh.dim * 8)
+        if args.summary_dtype == "f16tc":
+            # + the f64 rows of the uncertain candidates (per pass) + the anchor
+            # B-operand atoms (16 B per element, written and read once)
+            if res is not None and res.get("steps"):
+                b += res["rescored_rows"] / res["steps"] * sh.dim * 8
+            b += batch * sh.dim * 16 * 2
+        return b
 
     def step_bytes(res, select_every):
         a = L * attn_bytes_per_layer(res["ws_mean"], res["mean_fill"])
         e = batch * wl.vocab * 4
         app = batch * sh.dim * (2 * 2 + 2 * 8)
-        s = select_bytes(res["sel_stats"]) if select_every else 0.0
+        s = select_bytes(res["sel_stats"], res) if select_every else 0.0
         return a + e + app + s
 
     results = {}
@@ -327,7 +351,7 @@ def run_gpu(args):
     k4_tiles = int(phys_now.size) * sh.kv_heads
     k4_unique_tiles = int(np.unique(phys_now).size) * sh.kv_heads
     attn_launch_bytes = attn_bytes_per_layer(ws_now, fill_now)
-    sel_call_bytes = select_bytes(st.sel_stats.cpu().numpy())
+    sel_call_bytes = select_bytes(st.sel_stats.cpu().numpy(), results["select_every_step"])
 
     # ---- e2e through the public step API with host buffers (pinned),
     # headline variant.  Every step's inputs are copied host->device and its
@@ -650,7 +674,7 @@ def main():
     ap.add_argument("--impl", default="chess", choices=["chess", "reference"])
     ap.add_argument("--config", default="cfg3")
     ap.add_argument("--batch", type=int, default=None)
-    ap.add_argument("--summary-dtype", default="f32", choices=["f32", "f64", "bf16"])
+    ap.add_argument("--summary-dtype", default="f32", choices=["f32", "f64", "bf16", "f16tc"])
     ap.add_argument("--full-scan", action="store_true")
     ap.add_argument("--headline-only", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")

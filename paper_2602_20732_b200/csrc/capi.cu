@@ -29,6 +29,7 @@ int launch_reset(const ChessState&, const uint8_t*, cudaStream_t);
 int launch_append(const ChessState&, const Workspace&, const void*, const void*, int64_t,
                   const uint8_t*, cudaStream_t, int64_t col0 = 0, int64_t ncols = -1, int post = 0);
 int launch_seal(const ChessState&, const Workspace&, cudaStream_t);
+int launch_select_tc_level(const ChessState&, const Workspace&, const SelParams&, int, cudaStream_t);
 int launch_build(const ChessState&, const int32_t*, cudaStream_t);
 int launch_from_vectors(const ChessState&, int, const double*, int, int64_t, const int32_t*,
                         cudaStream_t);
@@ -141,6 +142,16 @@ size_t workspace_layout(const ChessDims& d, void* base, Workspace* ws) {
   const size_t o_ent_part = take(b * kEntSplit * 3 * 8);
   const size_t o_app = take(b * 4);
   const size_t o_seal = take(b * 4);
+  // tensor-core scan state (summary_dtype 3 only)
+  const bool tcs = d.summary_dtype == kSummaryTc;
+  const int64_t nkb_pad = tcs ? (d.ld / 64 + kTcKbs - 1) / kTcKbs * kTcKbs : 0;
+  const size_t o_mpend = take(b * 4);
+  const size_t o_atile = take(tcs ? b * nkb_pad * 1024 : 0);
+  const size_t o_astats = take(tcs ? b * nsl * 4 * 8 : 0);
+  const size_t o_aexp = take(tcs ? b * nsl * 4 : 0);
+  const size_t o_cls = take(tcs ? b * mr * 4 : 0);
+  const size_t o_unc = take(tcs ? b * mr * 4 : 0);
+  const size_t o_umeta = take(b * 4 * 4);
   if (ws && base) {
     uint8_t* p = reinterpret_cast<uint8_t*>(base);
     ws->sel_done = reinterpret_cast<int32_t*>(p + o_sel_done);
@@ -159,6 +170,14 @@ size_t workspace_layout(const ChessDims& d, void* base, Workspace* ws) {
     ws->ent_part = reinterpret_cast<double*>(p + o_ent_part);
     ws->append_done = reinterpret_cast<int32_t*>(p + o_app);
     ws->seal_done = reinterpret_cast<int32_t*>(p + o_seal);
+    ws->mirror_pend = reinterpret_cast<int32_t*>(p + o_mpend);
+    ws->anc_tile = tcs ? p + o_atile : nullptr;
+    ws->anc_stats = tcs ? reinterpret_cast<double*>(p + o_astats) : nullptr;
+    ws->anc_exp = tcs ? reinterpret_cast<int32_t*>(p + o_aexp) : nullptr;
+    ws->cls = tcs ? reinterpret_cast<int32_t*>(p + o_cls) : nullptr;
+    ws->unc = tcs ? reinterpret_cast<int32_t*>(p + o_unc) : nullptr;
+    ws->unc_meta = reinterpret_cast<int32_t*>(p + o_umeta);
+    ws->nkb_pad = (int32_t)nkb_pad;
     ws->n_slices = (int32_t)nsl;
     ws->attn_ctas = std::min(attn_ctas_for(d), kAttnCtasMax);
   }
@@ -186,7 +205,14 @@ static int validate(const ChessDims& d) {
     return fail(CHESS_ERR_CONFIG, "max_ws (%d) must be >= max_pages (%d): a working set may hold every page",
                 d.max_ws, d.max_pages);
   if (d.n_phys < 1) return fail(CHESS_ERR_CONFIG, "store capacity must be >= 1 page");
-  if (d.summary_dtype < 0 || d.summary_dtype > 2) return fail(CHESS_ERR_CONFIG, "summary_dtype must be 0 (f32), 1 (f64) or 2 (bf16)");
+  if (d.summary_dtype < 0 || d.summary_dtype > 3)
+    return fail(CHESS_ERR_CONFIG, "summary_dtype must be 0 (f32), 1 (f64), 2 (bf16) or 3 (fp16 tensor-core scan)");
+  if (d.summary_dtype == kSummaryTc) {
+    // row groups of 8 consecutive children = one TMA box / MMA row block
+    if (d.pages_per_chunk % 8 || d.chunks_per_grid % 8)
+      return fail(CHESS_ERR_UNSUPPORTED, "summary_dtype 3 needs hierarchy fan-outs that are multiples of 8");
+    if (d.ld % 64) return fail(CHESS_ERR_CONFIG, "summary_dtype 3 needs ld %% 64 == 0 (64-element K blocks)");
+  }
   return CHESS_OK;
 }
 
@@ -349,6 +375,47 @@ int chess_select(const ChessState* st, const ChessSelectCfg* cfg, void* stream) 
   SelParams prm;
   if ((rc = select_params(cfg, &prm))) return rc;
   return launch_select(*st, ws, prm, 0, (cudaStream_t)stream);
+}
+
+// ---- debug / test entries (not in include/chess_b200.h) -------------------
+
+// summary_dtype 3: anchor split + tensor-core scan of one level (conditional
+// cascade), stopping before the exact rescoring launch
+extern "C" int chess_debug_select_tc_level(const ChessState* st, const ChessSelectCfg* cfg, int32_t level,
+                                           void* stream) {
+  Workspace ws;
+  int rc = state_ws(st, &ws);
+  if (rc) return rc;
+  if (st->d.summary_dtype != kSummaryTc) return fail(CHESS_ERR_CONFIG, "summary_dtype 3 only");
+  if (level < 0 || level > 2) return fail(CHESS_ERR_VALUE, "level %d", level);
+  SelParams prm;
+  if ((rc = select_params(cfg, &prm))) return rc;
+  return launch_select_tc_level(*st, ws, prm, level, (cudaStream_t)stream);
+}
+
+// Copy slot `slot`'s certified intervals of the last tensor-core level tail
+// (lo in ws.scores, hi in the first slice partial), classes, the
+// {uncertain, seats left, candidates, cumulative rescored} counters and the
+// level's candidate ids (level > 0) to host buffers (synchronous; any pointer
+// may be NULL).
+extern "C" int chess_debug_tc_read(const ChessState* st, int32_t slot, int32_t level, int32_t n, double* lo,
+                                   double* hi, int32_t* cls, int32_t* meta, int32_t* cand) {
+  Workspace ws;
+  int rc = state_ws(st, &ws);
+  if (rc) return rc;
+  if (st->d.summary_dtype != kSummaryTc) return fail(CHESS_ERR_CONFIG, "summary_dtype 3 only");
+  const int64_t mr = max_rows(st->d);
+  if (slot < 0 || slot >= st->d.batch || n < 0 || n > mr) return fail(CHESS_ERR_INDEX, "slot/n out of range");
+  cudaDeviceSynchronize();
+  if (lo) cudaMemcpy(lo, ws.scores + slot * mr, n * sizeof(double), cudaMemcpyDeviceToHost);
+  if (hi)
+    cudaMemcpy2D(hi, sizeof(double), ws.part + slot * mr * ws.n_slices, ws.n_slices * sizeof(double),
+                 sizeof(double), n, cudaMemcpyDeviceToHost);
+  if (cls) cudaMemcpy(cls, ws.cls + slot * mr, n * sizeof(int32_t), cudaMemcpyDeviceToHost);
+  if (meta) cudaMemcpy(meta, ws.unc_meta + 4 * slot, 4 * sizeof(int32_t), cudaMemcpyDeviceToHost);
+  if (cand && level > 0)
+    cudaMemcpy(cand, ws.cand + (slot * 3 + level) * mr, n * sizeof(int32_t), cudaMemcpyDeviceToHost);
+  return check_launch("debug_tc_read");
 }
 
 // rows a level can have for one slot: its exchange row stride must hold them

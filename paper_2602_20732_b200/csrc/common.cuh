@@ -42,9 +42,15 @@ __host__ __device__ inline int64_t max_rows(const ChessDims& d) { return d.max_p
 // bulk copy (f32 mirrors: 4096, f64 rows: 2048), so a ring of 12 stages
 // holds 1.5 items of 8 rows.
 constexpr int kScanSliceBytes = 16384;
-// summary_dtype: 0 f32 mirrors, 1 f64 (no mirrors), 2 bf16 mirrors
+// summary_dtype: 0 f32 mirrors, 1 f64 (no mirrors), 2 bf16 mirrors,
+// 3 fp16 mirrors scored on tcgen05 with certified bounds + exact f64
+// rescoring of the rows near each level's cut (k_select_tc.cuh).  For 3 the
+// element size below is that of the rows the exact (rescoring / short-row)
+// scan reads: f64.
+constexpr int kSummaryTc = 3;
+constexpr int kTcKbs = 4;  // 64-element K blocks per tensor-core scan stage
 __host__ __device__ constexpr int summary_elem_bytes(int summary_dtype) {
-  return summary_dtype == 0 ? 4 : (summary_dtype == 1 ? 8 : 2);
+  return summary_dtype == 0 ? 4 : (summary_dtype == 2 ? 2 : 8);
 }
 __host__ __device__ constexpr int scan_slice(int summary_dtype) { return kScanSliceBytes / summary_elem_bytes(summary_dtype); }
 constexpr int kScanRows = 8;       // rows per work item
@@ -78,6 +84,15 @@ struct Workspace {
   double* ent_part;      // [batch][kEntSplit][3]
   int32_t* append_done;  // [batch]
   int32_t* seal_done;    // [batch]
+  // summary_dtype 3 (tensor-core scan, k_select_tc.cuh)
+  int32_t* mirror_pend;  // [batch] 1 + page sealed by the last seal/fold (0: none)
+  uint8_t* anc_tile;     // [batch][nkb_pad][1024] anchor hi/lo as swizzled fp16 B atoms
+  double* anc_stats;     // [batch][n_slices][4] per-slice sum a^2, sum rem^2, sum (|hi|+|lo|)^2
+  int32_t* anc_exp;      // [batch][n_slices] power-of-two scale of the slice's anchor
+  int32_t* cls;          // [batch][max_rows] certification: 0 out, 1 certainly in, 2 uncertain
+  int32_t* unc;          // [batch][max_rows] candidate positions to rescore exactly
+  int32_t* unc_meta;     // [batch][4] uncertain count, seats left for them, candidates
+  int32_t nkb_pad;       // 64-element K blocks per row, padded to the stage size
   int32_t attn_ctas;
   int32_t n_slices;
 };
@@ -101,6 +116,7 @@ struct SelParams {
   int32_t force_all;
   int32_t mode;  // debug (CHESS_SELECT_MODE): 0 normal, 1 no math, 2 no loads
   int32_t defer_ws;  // leave working sets to chess_flush_working_sets (concurrent step)
+  int32_t rescore;   // summary_dtype 3: exact f64 pass over the level's uncertain rows
   // KV-head shard: when set, the level's tail stops after the
   // fixed-order slice reduction and exports this rank's PARTIAL scores to
   // xout[slot * xld + candidate]; select_combine_kernel finishes the level.
@@ -130,6 +146,8 @@ __device__ __forceinline__ float2 bf2x2f(uint32_t packed) {
 
 // write a scanned-summary mirror element (the *_vec32 buffers hold f32 rows
 // for summary_dtype 0 and bf16 rows for 2; f64 scans read the f64 rows)
+// (summary_dtype 3: the fp16 mirror and its row bounds are written by
+// mirror16_kernel from the finished f64 rows, k_index.cu)
 __device__ __forceinline__ void store_mirror(float* base, int64_t i, double v, int summary_dtype) {
   if (summary_dtype == 0) base[i] = (float)v;
   else if (summary_dtype == 2) reinterpret_cast<__nv_bfloat16*>(base)[i] = __double2bfloat16(v);

@@ -13,6 +13,8 @@
 // selection scan.
 #include <algorithm>
 
+#include <cuda_fp16.h>
+
 #include "common.cuh"
 
 namespace chess {
@@ -278,10 +280,13 @@ __global__ void __launch_bounds__(kNT) append_kernel(ChessState st, const __nv_b
 // K1 seal: fold the just-sealed tail page of each slot (hierarchy.py:102-136)
 // grid: (ceil(ld / kNT), batch); one element per thread.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(kNT) seal_kernel(ChessState st, int32_t* done) {
+__global__ void __launch_bounds__(kNT) seal_kernel(ChessState st, int32_t* done, int32_t* pend) {
   __shared__ int s_last;
   const int s = blockIdx.y;
-  if (!st.sealed[s]) return;
+  if (!st.sealed[s]) {
+    if (pend && blockIdx.x == 0 && threadIdx.x == 0) pend[s] = 0;  // no fp16 mirror rows owed
+    return;
+  }
   const ChessDims& d = st.d;
   const int64_t ld = d.ld;
   const int P = st.num_sealed[s];  // logical index of the sealing page
@@ -320,6 +325,7 @@ __global__ void __launch_bounds__(kNT) seal_kernel(ChessState st, int32_t* done)
   __syncthreads();
   if (s_last && threadIdx.x == 0) {
     done[s] = 0;
+    if (pend) pend[s] = P + 1;  // mirror16_kernel refreshes this page's rows
     st.num_sealed[s] = P + 1;
     st.sealed[s] = 0;
     // device pool: the slot's next append opens page num_pages — reserve it now
@@ -341,7 +347,7 @@ __device__ __forceinline__ double ld_elem<__nv_bfloat16>(const __nv_bfloat16* p)
 template <typename T>
 __global__ void __launch_bounds__(kNT) fold_rows_kernel(ChessState st, int s, const T* rows,
                                                         int n_rows, int64_t row_stride,
-                                                        int32_t* done) {
+                                                        int32_t* done, int32_t* pend) {
   __shared__ int s_last;
   const ChessDims& d = st.d;
   const int64_t ld = d.ld;
@@ -388,7 +394,89 @@ __global__ void __launch_bounds__(kNT) fold_rows_kernel(ChessState st, int s, co
   __syncthreads();
   if (s_last && threadIdx.x == 0) {
     done[s] = 0;
+    if (pend) pend[s] = P + 1;
     st.num_sealed[s] = P + 1;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K1m: fp16 mirror rows + certified row bounds (summary_dtype 3).
+// The tensor-core scan (k_select_tc.cuh) scores h = fp16(v) (round to
+// nearest) of every f64 summary row v; its certificates need, per row,
+//   err = ||v - h||_2  and  nrm = ||h||_2
+// (both rounded up), kept in the row's stash right after its ld halves (the
+// mirror buffers have the f32 row pitch, 4*ld bytes).  One CTA per (row,
+// slot); fixed thread partition and reduction tree, so the bounds are
+// deterministic.  An fp16 overflow makes err infinite: the row is then
+// always rescored exactly, never mis-certified.
+// mode 0: the page pend[s]-1 just sealed and its chunk and grid (3 CTAs);
+// mode 1: every row of the slot's sealed index (bulk builds).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) mirror16_kernel(ChessState st, const int32_t* pend, int only_seq, int mode) {
+  const int s = only_seq >= 0 ? only_seq : blockIdx.y;
+  const ChessDims& d = st.d;
+  const int Nc = d.pages_per_chunk, Ng = d.chunks_per_grid;
+  int which, row;
+  if (mode == 0) {
+    const int P = pend[s] - 1;
+    if (P < 0) return;
+    which = blockIdx.x;
+    row = which == 0 ? P : (which == 1 ? P / Nc : P / Nc / Ng);
+  } else {
+    const int n = st.num_sealed[s];
+    const int C = (n + Nc - 1) / Nc, G = (C + Ng - 1) / Ng;
+    const int r = blockIdx.x;
+    if (r < n) which = 0, row = r;
+    else if (r < n + C) which = 1, row = r - n;
+    else if (r < n + C + G) which = 2, row = r - n - C;
+    else return;
+  }
+  const int64_t rows = which == 0 ? (int64_t)d.max_pages : (which == 1 ? max_chunks(d) : max_grids(d));
+  const int64_t ri = (int64_t)s * rows + row;
+  const double* src = (which == 0 ? st.page_vec64 : (which == 1 ? st.chunk_vec64 : st.grid_vec64)) + ri * d.ld;
+  float* mrow = (which == 0 ? st.page_vec32 : (which == 1 ? st.chunk_vec32 : st.grid_vec32)) + ri * d.ld;
+  __half* dst = reinterpret_cast<__half*>(mrow);
+  double e2 = 0.0, n2 = 0.0;
+  for (int64_t j = (int64_t)threadIdx.x * 4; j < d.ld; j += 256 * 4) {
+    const double2 a = *reinterpret_cast<const double2*>(src + j);
+    const double2 b = *reinterpret_cast<const double2*>(src + j + 2);
+    const double v[4] = {a.x, a.y, b.x, b.y};
+    __half h[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      h[q] = __double2half(v[q]);
+      const double hd = (double)__half2float(h[q]);
+      const double dl = v[q] - hd;
+      e2 = __fma_rn(dl, dl, e2);
+      n2 = __fma_rn(hd, hd, n2);
+    }
+    uint2 w;
+    w.x = (uint32_t)__half_as_ushort(h[0]) | ((uint32_t)__half_as_ushort(h[1]) << 16);
+    w.y = (uint32_t)__half_as_ushort(h[2]) | ((uint32_t)__half_as_ushort(h[3]) << 16);
+    *reinterpret_cast<uint2*>(dst + j) = w;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    e2 += __shfl_xor_sync(0xffffffffu, e2, o);
+    n2 += __shfl_xor_sync(0xffffffffu, n2, o);
+  }
+  __shared__ double s_e[8], s_n[8];
+  if ((threadIdx.x & 31) == 0) {
+    s_e[threadIdx.x >> 5] = e2;
+    s_n[threadIdx.x >> 5] = n2;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double e = 0.0, n = 0.0;
+    for (int w = 0; w < 8; ++w) {
+      e += s_e[w];
+      n += s_n[w];
+    }
+    // sums of <= 2^31 non-negative terms: relative error < 2^-21 is far
+    // inside the (1 + 2^-20) inflation; sqrt is correctly rounded
+    double* stash = reinterpret_cast<double*>(reinterpret_cast<uint8_t*>(mrow) + 2 * d.ld);
+    stash[0] = sqrt(e) * (1.0 + 0x1p-20);
+    stash[1] = sqrt(n) * (1.0 + 0x1p-20);
   }
 }
 
@@ -621,20 +709,29 @@ int launch_append(const ChessState& st, const Workspace& ws, const void* k_rows,
 
 int launch_seal(const ChessState& st, const Workspace& ws, cudaStream_t stream) {
   dim3 grid((unsigned)((st.d.ld + kNT - 1) / kNT), st.d.batch);
-  seal_kernel<<<grid, kNT, 0, stream>>>(st, ws.seal_done);
-  return check_launch("summary_seal");
+  const bool tcs = st.d.summary_dtype == kSummaryTc;
+  seal_kernel<<<grid, kNT, 0, stream>>>(st, ws.seal_done, tcs ? ws.mirror_pend : nullptr);
+  int rc = check_launch("summary_seal");
+  if (rc || !tcs) return rc;
+  mirror16_kernel<<<dim3(3, st.d.batch), 256, 0, stream>>>(st, ws.mirror_pend, -1, 0);
+  return check_launch("mirror16");
 }
 
 int launch_fold(const ChessState& st, const Workspace& ws, int seq, const void* rows, int dtype,
                 int n_rows, int64_t row_stride, cudaStream_t stream) {
   const unsigned grid = (unsigned)((st.d.ld + kNT - 1) / kNT);
+  const bool tcs = st.d.summary_dtype == kSummaryTc;
+  int32_t* pend = tcs ? ws.mirror_pend : nullptr;
   if (dtype == CHESS_F64)
-    fold_rows_kernel<double><<<grid, kNT, 0, stream>>>(st, seq, (const double*)rows, n_rows, row_stride, ws.seal_done);
+    fold_rows_kernel<double><<<grid, kNT, 0, stream>>>(st, seq, (const double*)rows, n_rows, row_stride, ws.seal_done, pend);
   else if (dtype == CHESS_F32)
-    fold_rows_kernel<float><<<grid, kNT, 0, stream>>>(st, seq, (const float*)rows, n_rows, row_stride, ws.seal_done);
+    fold_rows_kernel<float><<<grid, kNT, 0, stream>>>(st, seq, (const float*)rows, n_rows, row_stride, ws.seal_done, pend);
   else
-    fold_rows_kernel<__nv_bfloat16><<<grid, kNT, 0, stream>>>(st, seq, (const __nv_bfloat16*)rows, n_rows, row_stride, ws.seal_done);
-  return check_launch("summary_fold");
+    fold_rows_kernel<__nv_bfloat16><<<grid, kNT, 0, stream>>>(st, seq, (const __nv_bfloat16*)rows, n_rows, row_stride, ws.seal_done, pend);
+  int rc = check_launch("summary_fold");
+  if (rc || !tcs) return rc;
+  mirror16_kernel<<<dim3(3, 1), 256, 0, stream>>>(st, ws.mirror_pend, seq, 0);
+  return check_launch("mirror16");
 }
 
 int launch_build(const ChessState& st, const int32_t* n_pages, cudaStream_t stream) {
@@ -645,7 +742,10 @@ int launch_build(const ChessState& st, const int32_t* n_pages, cudaStream_t stre
   if (rc) return rc;
   dim3 g2((unsigned)((st.d.ld + kNT - 1) / kNT), st.d.batch);
   build_finish_kernel<<<g2, kNT, 0, stream>>>(st, n_pages, -1);
-  return check_launch("summary_build_finish");
+  rc = check_launch("summary_build_finish");
+  if (rc || st.d.summary_dtype != kSummaryTc) return rc;
+  mirror16_kernel<<<dim3((unsigned)max_rows(st.d), st.d.batch), 256, 0, stream>>>(st, nullptr, -1, 1);
+  return check_launch("mirror16");
 }
 
 int launch_from_vectors(const ChessState& st, int seq, const double* rows, int n,
@@ -663,7 +763,10 @@ int launch_from_vectors(const ChessState& st, int seq, const double* rows, int n
     if (rc) return rc;
   }
   build_finish_kernel<<<dim3(gx, 1), kNT, 0, stream>>>(st, n_dev, seq);
-  return check_launch("from_vectors_finish");
+  int rc = check_launch("from_vectors_finish");
+  if (rc || d.summary_dtype != kSummaryTc) return rc;
+  mirror16_kernel<<<dim3((unsigned)max_rows(d), 1), 256, 0, stream>>>(st, nullptr, seq, 1);
+  return check_launch("mirror16");
 }
 
 int launch_mean_rows(const void* rows, int dtype, int64_t n, int64_t dim, int64_t ld, double* out,

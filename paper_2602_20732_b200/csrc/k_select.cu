@@ -19,9 +19,12 @@
 // them in fixed slice order (deterministic), runs the radix top-k and writes
 // the next level's candidate list, or — at the page level — the semantic set,
 // working set and block table.
+#include <cudaTypedefs.h>
+
 #include <cstdlib>
 
 #include "common.cuh"
+#include "tc.cuh"
 
 namespace chess {
 
@@ -53,6 +56,7 @@ __device__ __forceinline__ int level_rows(const ChessState& st, const Workspace&
   if (!fired(st, prm, s)) return 0;
   const LevelShape sh = shape_of(st, s);
   if (sh.P == 0) return 0;
+  if (prm.rescore) return ws.unc_meta[4 * s];  // uncertain rows of the tensor-core pass
   if (level == 0) return sh.G;
   if (level == 3) return sh.G + sh.C + sh.P;
   return ws.cand_n[4 * s + level];
@@ -156,6 +160,8 @@ __device__ void expand_children(const int* parents, int m, int fan, int total_ch
 
 __device__ void select_tail_topk(const ChessState& st, const Workspace& ws, const SelParams& prm,
                                  int s, int level, int n, TailSmem& sm);
+__device__ void tc_rescore_finish(const ChessState& st, const Workspace& ws, const SelParams& prm, int s, int lv,
+                                  TailSmem& sm);
 
 // Tail of one slot's level: fixed-order slice reduction of the partials into
 // ws.scores[s] (or, head-shard exchange mode, into prm.xout), then the top-k.
@@ -214,6 +220,10 @@ __device__ void select_tail(const ChessState& st, const Workspace& ws, const Sel
     return;
   }
   if (prm.xout) return;  // head shard: exchange, then select_combine_kernel finishes the level
+  if (prm.rescore) {
+    tc_rescore_finish(st, ws, prm, s, level, sm);
+    return;
+  }
   select_tail_topk(st, ws, prm, s, level, n, sm);
 }
 
@@ -496,7 +506,9 @@ __global__ void __launch_bounds__(kScanCTA, CHESS_SCAN_MINB) select_scan_kernel(
           const LevelShape sh = shape_of(st, s);
           const int64_t ebase = (int64_t)p.slice * SC::kSlice;
           bytes = (uint32_t)(min((int64_t)SC::kSlice, d.ld - ebase) * sizeof(T));
-          src = level_row_ptr<T>(st, ws, s, level, p.r0 + r, sh) + ebase;
+          // rescore mode: the row is the level candidate at an uncertain position
+          const int ci = prm.rescore ? __ldcg(&ws.unc[(int64_t)s * max_rows(d) + p.r0 + r]) : p.r0 + r;
+          src = level_row_ptr<T>(st, ws, s, level, ci, sh) + ebase;
         }
       }
     };
@@ -553,7 +565,7 @@ __global__ void __launch_bounds__(kScanCTA, CHESS_SCAN_MINB) select_scan_kernel(
   }
 
   // ===================== consumers =====================
-  if ((level == 0 || level == 3) && blockIdx.x == 0) handle_empty_slots(st, ws, prm, sm);
+  if ((level == 0 || level == 3) && blockIdx.x == 0 && !prm.rescore) handle_empty_slots(st, ws, prm, sm);
   int k = 0, buf = 0;
   int s = -1, contributed = 0, a_slice = -1;
   double a[SC::kPerThread];
@@ -1394,6 +1406,8 @@ __global__ void gather_pages_kernel(const int32_t* table, int n_pages, const int
   }
 }
 
+#include "k_select_tc.cuh"
+
 }  // namespace
 
 // ---------------------------------------------------------------------------
@@ -1440,6 +1454,86 @@ static int launch_flow(const ChessState& st, const Workspace& ws, const SelParam
   return check_launch("select_flow");
 }
 
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+// 3-D view of one level's fp16 mirror rows (summary_dtype 3): (64 elements,
+// rows, K blocks) with strides (f32 row pitch 4*ld B, 128 B); a box
+// (64, 8, kTcKbs) is 8 consecutive rows x 4 K blocks, landing as
+// [K block][8 rows][128 B] with 128B swizzle = four MMA atoms of one group.
+static int make_mirror_map(CUtensorMap* m, const float* base, int64_t rows, const ChessDims& d) {
+  auto fn = encode_fn();
+  if (!fn) return fail(CHESS_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[3] = {64, (cuuint64_t)rows, (cuuint64_t)(d.ld / 64)};
+  cuuint64_t strides[2] = {(cuuint64_t)d.ld * 4, 128};
+  cuuint32_t box[3] = {64, 8, (cuuint32_t)kTcKbs};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, const_cast<float*>(base), dims, strides, box, es,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(CHESS_ERR_CUDA, "cuTensorMapEncodeTiled (mirror) failed (%d)", (int)r);
+  return CHESS_OK;
+}
+
+static size_t tc_smem(int batch) {
+  return 1024 + (size_t)kTcStages * kTcStageBytes + (size_t)(2 * kTcStages + 2 * kTcAcc) * 8 + 16 +
+         (size_t)(2 * batch + 1) * sizeof(int);
+}
+
+// summary_dtype 3: anchor split, then per level the tensor-core scan and the
+// exact f64 rescoring of its uncertain rows (k_select_tc.cuh)
+static int launch_select_tc(const ChessState& st, const Workspace& ws, const SelParams& prm, cudaStream_t stream) {
+  const ChessDims& d = st.d;
+  anchor_prep_kernel<<<dim3((unsigned)ws.n_slices, (unsigned)d.batch), 256, 0, stream>>>(st, ws, prm);
+  int rc = check_launch("anchor_prep");
+  if (rc) return rc;
+  CUtensorMap mg, mc, mp;
+  if ((rc = make_mirror_map(&mg, st.grid_vec32, (int64_t)d.batch * max_grids(d), d))) return rc;
+  if ((rc = make_mirror_map(&mc, st.chunk_vec32, (int64_t)d.batch * max_chunks(d), d))) return rc;
+  if ((rc = make_mirror_map(&mp, st.page_vec32, (int64_t)d.batch * d.max_pages, d))) return rc;
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(select_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc_smem(kMaxBatch));
+    if ((rc = check_launch("select_tc smem attribute"))) return rc;
+    configured = true;
+  }
+  SelParams pr = prm;
+  pr.rescore = 1;
+  for (int level = 0; level < 3; ++level) {
+    select_tc_kernel<<<num_sms(), kTcCTA, tc_smem(d.batch), stream>>>(st, ws, prm, level, mg, mc, mp);
+    if ((rc = check_launch("select_tc"))) return rc;
+    if ((rc = launch_scan<double>(st, ws, pr, level, stream))) return rc;
+  }
+  return CHESS_OK;
+}
+
+// Debug / test entry: anchor split + the tensor-core scan of ONE level,
+// without the exact rescoring, so a test can read the certified intervals
+// (chess_debug_tc_read) before the next launch consumes them.
+int launch_select_tc_level(const ChessState& st, const Workspace& ws, const SelParams& prm, int level,
+                           cudaStream_t stream) {
+  const ChessDims& d = st.d;
+  anchor_prep_kernel<<<dim3((unsigned)ws.n_slices, (unsigned)d.batch), 256, 0, stream>>>(st, ws, prm);
+  int rc = check_launch("anchor_prep");
+  if (rc) return rc;
+  CUtensorMap mg, mc, mp;
+  if ((rc = make_mirror_map(&mg, st.grid_vec32, (int64_t)d.batch * max_grids(d), d))) return rc;
+  if ((rc = make_mirror_map(&mc, st.chunk_vec32, (int64_t)d.batch * max_chunks(d), d))) return rc;
+  if ((rc = make_mirror_map(&mp, st.page_vec32, (int64_t)d.batch * d.max_pages, d))) return rc;
+  cudaFuncSetAttribute(select_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc_smem(kMaxBatch));
+  select_tc_kernel<<<num_sms(), kTcCTA, tc_smem(d.batch), stream>>>(st, ws, prm, level, mg, mc, mp);
+  return check_launch("select_tc");
+}
+
 // persistent scan: one CTA per SM (192 KB TMA ring each), one launch per level
 int launch_select(const ChessState& st, const Workspace& ws, const SelParams& prm, int /*grid*/,
                   cudaStream_t stream) {
@@ -1448,6 +1542,11 @@ int launch_select(const ChessState& st, const Workspace& ws, const SelParams& pr
   // measured slower than three per-level launches (tools/select_micro.py:
   // cfg3 378 vs 308 us, cfg2 45 vs 38 us) — kept for further work.
   static const int flow_env = getenv("CHESS_SELECT_FLOW") ? atoi(getenv("CHESS_SELECT_FLOW")) : 0;
+  // tensor-core scan (summary_dtype 3) for the conditional cascade over long
+  // rows; full scans, head-shard exchanges and short rows use the exact f64 path
+  const bool tc_path = st.d.summary_dtype == kSummaryTc && !prm.full_scan && !prm.xout && !prm.xpeer &&
+                       st.d.ld * summary_elem_bytes(st.d.summary_dtype) > kSmallRowBytes;
+  if (tc_path) return launch_select_tc(st, ws, prm, stream);
   if (flow_env && !prm.full_scan && !prm.xout && !prm.xpeer && prm.mode == 0 && st.d.batch <= kFlowMaxBatch)
     return st.d.summary_dtype == 0 ? launch_flow<float>(st, ws, prm, stream)
            : st.d.summary_dtype == 2 ? launch_flow<__nv_bfloat16>(st, ws, prm, stream)

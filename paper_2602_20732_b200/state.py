@@ -34,7 +34,9 @@ class Shape:
     window_pages: int
     max_ws: int
     n_phys: int
-    summary_dtype: str = "f32"  # "f32" or "bf16" mirrors scanned, or "f64"
+    summary_dtype: str = "f32"  # "f32"/"bf16" mirrors scanned, "f64", or "f16tc"
+    # ("f16tc": fp16 mirrors scored on tcgen05 with certified bounds, rows near
+    # each level's cut rescored from f64 -> the f64 selection, k_select_tc.cuh)
 
     @property
     def dim(self) -> int:
@@ -42,7 +44,10 @@ class Shape:
 
     @property
     def ld(self) -> int:
-        # bf16 mirror rows must be 16-byte multiples for the scan's bulk copies
+        # bf16 mirror rows must be 16-byte multiples for the scan's bulk copies;
+        # the tensor-core scan reads 64-element K blocks
+        if self.summary_dtype == "f16tc":
+            return _round_up(self.dim, 64)
         return _round_up(self.dim, 8 if self.summary_dtype == "bf16" else 4)
 
     @property
@@ -52,6 +57,9 @@ class Shape:
     @property
     def max_grids(self) -> int:
         return math.ceil(self.max_chunks / self.chunks_per_grid)
+
+
+SUMMARY_DTYPES = {"f32": 0, "f64": 1, "bf16": 2, "f16tc": 3}
 
 
 class DecodeState:
@@ -84,8 +92,9 @@ class DecodeState:
         self.grid_sum64 = torch.zeros((b, s.max_grids, ld), **f64)
         self.chunk_vec64 = torch.zeros((b, s.max_chunks, ld), **f64)
         self.grid_vec64 = torch.zeros((b, s.max_grids, ld), **f64)
-        if s.summary_dtype in ("f32", "bf16"):
-            mdt = dict(f32) if s.summary_dtype == "f32" else dict(dtype=torch.bfloat16, device=dev)
+        if s.summary_dtype in ("f32", "bf16", "f16tc"):
+            # f16tc: fp16 rows + {err, nrm} stash inside the f32 row pitch
+            mdt = dict(f32) if s.summary_dtype != "bf16" else dict(dtype=torch.bfloat16, device=dev)
             self.page_vec32 = torch.zeros((b, s.max_pages, ld), **mdt)
             self.chunk_vec32 = torch.zeros((b, s.max_chunks, ld), **mdt)
             self.grid_vec32 = torch.zeros((b, s.max_grids, ld), **mdt)
@@ -122,7 +131,7 @@ class DecodeState:
         d.head_dim, d.page_size = s.head_dim, s.page_size
         d.pages_per_chunk, d.chunks_per_grid = s.pages_per_chunk, s.chunks_per_grid
         d.max_pages, d.window_pages, d.max_ws = s.max_pages, s.window_pages, s.max_ws
-        d.summary_dtype = {"f32": 0, "f64": 1, "bf16": 2}[s.summary_dtype]
+        d.summary_dtype = SUMMARY_DTYPES[s.summary_dtype]
         d.dim, d.ld, d.n_phys = s.dim, ld, s.n_phys
         lib = _lib.load()
         _lib.check(lib.chess_validate_dims(C.byref(d)), "validate_dims")
@@ -176,6 +185,13 @@ class DecodeState:
         if self.shape.summary_dtype in ("f32", "bf16"):
             return self.grid_vec32, self.chunk_vec32, self.page_vec32
         return self.grid_vec64, self.chunk_vec64, self.page_vec64
+
+    def mirror16(self, which: int):
+        """f16tc: (fp16 rows [b, rows, ld], stash f64 [b, rows, 2] = {err, nrm})
+        of the grid (0), chunk (1) or page (2) matrix (mirror16_kernel)."""
+        m = (self.grid_vec32, self.chunk_vec32, self.page_vec32)[which]
+        ld = self.shape.ld
+        return m.view(torch.float16)[..., :ld], m.view(torch.float64)[..., ld // 4: ld // 4 + 2]
 
     def bytes_allocated(self) -> int:
         tot = 0

@@ -114,8 +114,8 @@ class SyntheticDecode:
         dim = shape0.dim
         mc, mg = shape0.max_chunks, shape0.max_grids
         state_bytes = b * dim * 8 * (max_pages + 2 * mc + 2 * mg + 4)
-        if summary_dtype in ("f32", "bf16"):
-            state_bytes += b * dim * (4 if summary_dtype == "f32" else 2) * (max_pages + mc + mg)
+        if summary_dtype in ("f32", "bf16", "f16tc"):  # f16tc: fp16 rows in f32-pitch buffers
+            state_bytes += b * dim * (2 if summary_dtype == "bf16" else 4) * (max_pages + mc + mg)
         free, total = torch.cuda.mem_get_info(device)
         ring_bytes = ring * b * (c["vocab"] * 4 + L * c["q_heads"] * d * 2 * 2 + dim * 4)
         budget = kv_budget_gib * GIB if kv_budget_gib else free - state_bytes - ring_bytes - 12 * GIB

@@ -52,13 +52,24 @@ def test_validate_dims_and_workspace(lib):
     assert lib.chess_validate_dims(C.byref(d)) == _lib.OK
     assert lib.chess_workspace_bytes(C.byref(d)) > 0
     for bad in (dict(batch=0), dict(page_size=0), dict(pages_per_chunk=0), dict(window_pages=0),
-                dict(q_heads=12), dict(dim=7), dict(ld=1030), dict(n_phys=0), dict(summary_dtype=3)):
+                dict(q_heads=12), dict(dim=7), dict(ld=1030), dict(n_phys=0), dict(summary_dtype=4),
+                dict(summary_dtype=3, ld=1028)):
         d = _dims(**bad)
         rc = lib.chess_validate_dims(C.byref(d))
         assert rc == _lib.ERR_CONFIG, bad
         assert lib.chess_workspace_bytes(C.byref(d)) == 0
         with pytest.raises(ConfigurationError):
             _lib.check(rc, "validate")
+
+
+def test_tensor_core_summary_dims(lib):
+    """summary_dtype 3 (fp16 mirrors scored on tcgen05): 64-element K blocks
+    and 8-row groups of children; other fan-outs have no kernel instance."""
+    d = _dims(summary_dtype=3)
+    assert lib.chess_validate_dims(C.byref(d)) == _lib.OK
+    assert lib.chess_workspace_bytes(C.byref(_dims(summary_dtype=3))) > lib.chess_workspace_bytes(C.byref(_dims()))
+    d = _dims(summary_dtype=3, pages_per_chunk=4)
+    assert lib.chess_validate_dims(C.byref(d)) == _lib.ERR_UNSUPPORTED
 
 
 def test_status_mapping():
