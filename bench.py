@@ -442,7 +442,7 @@ def run_gpu(args):
         "higher_is_better": True,
         "scaling": "strong" if head else "weak",
         "vs_baseline": None,
-        "dtype": f"bf16 KV / {args.summary_dtype} summaries / f64 scores",
+        "dtype": DTYPES[args.summary_dtype],
         "data": "synthetic (planted-relevance keys, random-init shapes)",
         "config": {
             "workload": f"{cfg_name}: {DESCRIPTIONS[cfg_name]}",
@@ -665,6 +665,14 @@ def run_plumbing(args):
         dist.destroy_process_group()
 
 
+DTYPES = {
+    "f16tc": "bf16 KV / fp16 summary mirrors on tcgen05 (certified bounds) + exact f64 rescoring near each cut",
+    "f32": "bf16 KV / f32 summary mirrors / f64 scores",
+    "f64": "bf16 KV / f64 summaries / f64 scores",
+    "bf16": "bf16 KV / bf16 summary mirrors / f64 scores",
+}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=None,
@@ -674,7 +682,9 @@ def main():
     ap.add_argument("--impl", default="chess", choices=["chess", "reference"])
     ap.add_argument("--config", default="cfg3")
     ap.add_argument("--batch", type=int, default=None)
-    ap.add_argument("--summary-dtype", default="f32", choices=["f32", "f64", "bf16", "f16tc"])
+    ap.add_argument("--summary-dtype", default="f16tc", choices=["f32", "f64", "bf16", "f16tc"],
+                    help="f16tc (default): fp16 mirrors scored on tcgen05 with certified bounds, exact f64 "
+                         "rescoring near each cut (selections identical to the f64 scores)")
     ap.add_argument("--full-scan", action="store_true")
     ap.add_argument("--headline-only", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")

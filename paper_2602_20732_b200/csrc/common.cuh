@@ -48,7 +48,10 @@ constexpr int kScanSliceBytes = 16384;
 // element size below is that of the rows the exact (rescoring / short-row)
 // scan reads: f64.
 constexpr int kSummaryTc = 3;
-constexpr int kTcKbs = 4;  // 64-element K blocks per tensor-core scan stage
+#ifndef CHESS_TC_KBS
+#define CHESS_TC_KBS 4
+#endif
+constexpr int kTcKbs = CHESS_TC_KBS;  // 64-element K blocks per tensor-core scan stage
 __host__ __device__ constexpr int summary_elem_bytes(int summary_dtype) {
   return summary_dtype == 0 ? 4 : (summary_dtype == 2 ? 2 : 8);
 }

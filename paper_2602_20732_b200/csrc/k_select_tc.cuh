@@ -38,9 +38,16 @@ constexpr int kTcSliceKb = kScanSliceBytes / 8 / 64;   // 32 K blocks = the f64 
 constexpr int kTcStageA = kTcGroups * kTcKbs * 1024;   // 64 KB of rows
 constexpr int kTcStageB = kTcKbs * 1024;               // 4 KB of anchor atoms
 constexpr int kTcStageBytes = kTcStageA + kTcStageB;
-constexpr int kTcStages = 3;
-constexpr int kTcAcc = 8;                              // TMEM accumulation windows in flight
-constexpr int kTcTmemCols = 64;                        // kTcAcc x N = 8 columns
+#ifndef CHESS_TC_ACC
+#define CHESS_TC_ACC 8
+#endif
+// as many stages as fit beside the tail's static shared memory (13.7 KB),
+// the barriers and the per-slot tables of kMaxBatch slots (<= 16 stages)
+constexpr int kTcStagesRaw = 209000 / kTcStageBytes;
+constexpr int kTcStages = kTcStagesRaw > 16 ? 16 : kTcStagesRaw;
+constexpr int kTcAcc = CHESS_TC_ACC;                   // TMEM accumulation windows in flight
+constexpr int kTcTmemCols = kTcAcc * 8 <= 32 ? 32 : (kTcAcc * 8 <= 64 ? 64 : (kTcAcc * 8 <= 128 ? 128 : 256));
+static_assert(kTcStages >= 2, "tensor-core scan ring too shallow");
 constexpr int kTcCTA = kNT + 64;                       // 8 epilogue/tail warps + TMA warp + MMA warp
 constexpr int kTcProducerWarp = kWarps, kTcMmaWarp = kWarps + 1;
 constexpr uint32_t kTcIdesc = tc::idesc_f16(128, 8, 0);
