@@ -19,7 +19,7 @@ BUILD = PKG_DIR / "_build"
 LIB = PKG_DIR / "libchess_b200.so"
 TRACE_LIB = PKG_DIR / "libchess_b200_trace.so"
 SOURCES = ["capi.cu", "k_index.cu", "k_select.cu", "k_attn.cu", "k_entropy.cu"]
-HEADERS = [CSRC / "common.cuh", CSRC / "tc.cuh", CSRC / "k_select_tc.cuh", REPO / "include" / "chess_b200.h"]
+HEADERS = [CSRC / "common.cuh", CSRC / "tc.cuh", CSRC / "k_select_tc.cuh", CSRC / "k_attn_tc.cuh", REPO / "include" / "chess_b200.h"]
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

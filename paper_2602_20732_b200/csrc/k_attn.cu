@@ -33,6 +33,7 @@
 #include <cstdlib>
 
 #include "common.cuh"
+#include "tc.cuh"
 
 namespace chess {
 
@@ -1000,6 +1001,8 @@ __global__ void __launch_bounds__(kThreads, CPS)
   }
 }
 
+#include "k_attn_tc.cuh"
+
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   if (!fn) {
@@ -1018,13 +1021,15 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 // layers) with strides (2 B, HD*2 B, 128 B, pool bytes).  One box
 // (64, B, HD/64, 1) is a whole (page, head) K or V tile, landing in smem as
 // [column block][B rows][128 B] with 128B swizzle — one TMA op per tile.
-int make_kv_map(CUtensorMap* m, const void* base, const ChessDims& d) {
+// cb_box = 1 (tensor-core K4): one box per (page, column block), so a
+// group's pages land column block by column block.
+int make_kv_map(CUtensorMap* m, const void* base, const ChessDims& d, int cb_box = 0) {
   auto fn = encode_fn();
   if (!fn) return fail(CHESS_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
   const cuuint64_t rows = (cuuint64_t)d.n_phys * d.kv_heads * d.page_size;
   cuuint64_t dims[4] = {64, rows, (cuuint64_t)d.head_dim / 64, (cuuint64_t)d.layers};
   cuuint64_t strides[3] = {(cuuint64_t)d.head_dim * 2, 128, rows * d.head_dim * 2};
-  cuuint32_t box[4] = {64, (cuuint32_t)d.page_size, (cuuint32_t)d.head_dim / 64, 1};
+  cuuint32_t box[4] = {64, (cuuint32_t)d.page_size, (cuuint32_t)(cb_box ? cb_box : d.head_dim / 64), 1};
   cuuint32_t es[4] = {1, 1, 1, 1};
   CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides, box,
                   es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -1124,12 +1129,58 @@ template <int HD, int GQ, int B, int CPS>
 int launch_grid(const ChessState& st, const Workspace& ws, const AttnArgs& args, int nctas,
                 cudaStream_t stream);
 
+// Tensor-core K4 (k_attn_tc.cuh): one CTA per SM, piece mode / stream-K.
+template <int GQ, int B>
+int launch_tc(const ChessState& st, const Workspace& ws, const AttnArgs& args, int nctas, cudaStream_t stream) {
+  static bool configured = false;
+  auto kfn = args.n_peer ? sparse_decode_tc_kernel<GQ, B, true> : sparse_decode_tc_kernel<GQ, B, false>;
+  if (!configured) {
+    cudaFuncAttributes fa;  // load both instances now (see cluster_size_for)
+    cudaFuncGetAttributes(&fa, sparse_decode_tc_kernel<GQ, B, true>);
+    cudaFuncGetAttributes(&fa, sparse_decode_tc_kernel<GQ, B, false>);
+    cudaFuncSetAttribute(sparse_decode_tc_kernel<GQ, B, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)tca::kSmem);
+    cudaFuncSetAttribute(sparse_decode_tc_kernel<GQ, B, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)tca::kSmem);
+    configured = true;
+  }
+  CUtensorMap km, vm;
+  int rc = make_kv_map(&km, st.k_pool, st.d, 1);
+  if (rc) return rc;
+  rc = make_kv_map(&vm, st.v_pool, st.d, 1);
+  if (rc) return rc;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(std::min(nctas, num_sms()));
+  cfg.blockDim = dim3(tca::kThreads);
+  cfg.dynamicSmemBytes = tca::kSmem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  static const bool no_pdl = getenv("CHESS_ATTN_NOPDL") != nullptr;  // debug A/B
+  cfg.numAttrs = no_pdl ? 0 : 1;
+  cudaLaunchKernelEx(&cfg, kfn, st, ws, args, km, vm);
+  return check_launch("sparse_decode_tc");
+}
+
 template <int HD, int GQ, int B>
 int launch_inst(const ChessState& st, const Workspace& ws, const AttnArgs& args_in, int nctas,
                 cudaStream_t stream) {
   AttnArgs args = args_in;
   const int segs = st.d.batch * st.d.kv_heads;
   args.cl = args.mode == 7 ? 0 : cluster_size_for<HD, GQ, B>(segs);
+  // CHESS_ATTN_TC: 0 (default) mma.sync consumer; 1 tensor-core consumer
+  // (k_attn_tc.cuh) wherever cluster mode is not chosen; 2 everywhere.
+  // Measured on B200 (profiles/r02/k4_tc/): a tcgen05.mma of kind::f16 costs
+  // ~150 cycles whatever N (8..128) and M (64, 128) are, so the decode shape
+  // (N = GQA heads = 4-8) runs the tensor pipe at ~1/30 of its rate; QK + PV
+  // take 4 MMAs per 32-token page = ~600 cycles per page, above the mma.sync
+  // consumer's ~500: cfg3 K4 18.96 vs 18.01 us, cfg5 20.8 vs 11.6, cfg4 54.7
+  // vs 45.7, cfg2 12.4 vs 3.2.
+  static const int tc_env = getenv("CHESS_ATTN_TC") ? atoi(getenv("CHESS_ATTN_TC")) : 0;
+  if constexpr (HD == 128 && (B == 16 || B == 32))
+    if (tc_env && args.mode == 0 && (tc_env == 2 || args.cl == 0)) return launch_tc<GQ, B>(st, ws, args, nctas, stream);
   if (args.cl) return launch_cluster<HD, GQ, B>(st, ws, args, segs, stream);
   // stream-K regime: two CTAs per SM over half-depth rings
   static const int cps_env = getenv("CHESS_ATTN_CPS") ? atoi(getenv("CHESS_ATTN_CPS")) : 0;  // A/B
@@ -1311,6 +1362,11 @@ int launch_gather_finish(uint32_t* const* flags, uint32_t* my_flags, int world, 
 
 // Debug only (not part of include/chess_b200.h): copy the per-CTA timeline of
 // the last sparse_decode launch of each layer parity, [2][256][16] u64 (ns; [8],[9] SM clocks).
+// tensor-core K4 per-group timeline (CHESS_TRACE builds; [8 CTAs][16 groups][8 events] clock64)
+extern "C" int chess_debug_attn_tc_trace(unsigned long long* host_out) {
+  return cudaMemcpyFromSymbol(host_out, chess::g_tca_trace, sizeof(chess::g_tca_trace)) == cudaSuccess ? 0 : 8;
+}
+
 extern "C" int chess_debug_attn_trace(unsigned long long* host_out) {
   return cudaMemcpyFromSymbol(host_out, chess::g_attn_trace, sizeof(chess::g_attn_trace)) == cudaSuccess ? 0 : 8;
 }

@@ -40,6 +40,28 @@ __host__ __device__ constexpr uint32_t idesc_f16(int M, int N, int ab_fmt) {
          ((uint32_t)(M >> 4) << 24);
 }
 
+// General shared-memory descriptor: layout 2 = SWIZZLE_128B, 0 = no swizzle
+// ("interleave": 8 x 16-byte core matrices).  K-major SW128: lbo unused,
+// sbo = 8-row group stride.  MN-major SW128: lbo = stride between 64-element
+// MN blocks, sbo = 8-row K group stride.  MN-major no-swizzle: 8 MN elements
+// contiguous (16 B), K rows 16 B apart, lbo = stride between 8-row K groups.
+// (Verified on B200 by tools/tc_attn_probe.cu.)
+__device__ __forceinline__ uint64_t smem_desc(uint32_t smem_addr, uint32_t lbo_bytes, uint32_t sbo_bytes,
+                                              uint32_t layout) {
+  uint64_t d = 0;
+  d |= (uint64_t)((smem_addr >> 4) & 0x3fffu);
+  d |= (uint64_t)((lbo_bytes >> 4) & 0x3fffu) << 16;
+  d |= (uint64_t)((sbo_bytes >> 4) & 0x3fffu) << 32;
+  d |= (uint64_t)1u << 46;
+  d |= (uint64_t)layout << 61;
+  return d;
+}
+
+// kind::f16 instruction descriptor with operand majors (0 = K-major, 1 = MN-major)
+__host__ __device__ constexpr uint32_t idesc_f16_major(int M, int N, int ab_fmt, int a_mn, int b_mn) {
+  return idesc_f16(M, N, ab_fmt) | ((uint32_t)a_mn << 15) | ((uint32_t)b_mn << 16);
+}
+
 // D[tmem] (+)= A[smem] * B[smem]^T, issued by one thread for the CTA.
 __device__ __forceinline__ void mma_f16_ss(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
                                            uint32_t accumulate) {
@@ -85,6 +107,18 @@ __device__ __forceinline__ void tmem_ld_x2(uint32_t taddr, float& c0, float& c1)
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
   c0 = __uint_as_float(r0);
   c1 = __uint_as_float(r1);
+}
+
+// Eight consecutive f32 columns of this thread's TMEM lane (then wait::ld).
+__device__ __forceinline__ void tmem_ld_x8(uint32_t taddr, float (&v)[8]) {
+  uint32_t r[8];
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "r"(taddr)
+               : "memory");
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
 }
 
 // 3-D tensor TMA load completing on an mbarrier (SASS: UTMALDG).

@@ -30,7 +30,7 @@ def _resources():
 
 def test_k4_arguments_stay_in_the_parameter_bank():
     res = _resources()
-    k4 = {k: v for k, v in res.items() if "sparse_decode_kernel" in k}
+    k4 = {k: v for k, v in res.items() if "sparse_decode_kernel" in k or "sparse_decode_tc_kernel" in k}
     assert k4
     for name, st in k4.items():
         assert st.get("STACK", 0) <= 64, (name, st)

@@ -3,6 +3,8 @@
 
 import ctypes
 
+import os
+
 import numpy as np
 import pytest
 import torch
@@ -127,6 +129,11 @@ ATTN_CASES = [
     (128, 32, 8, 32, 16, [47] * 16, [32, 1, 5, 31] * 4),
     # batch x kv_heads > SMs: stream-K split segments, two CTAs per SM
     (128, 32, 8, 32, 24, [1, 2, 3, 5, 8, 13, 21, 34] * 3, [32, 1, 17, 9] * 6),
+    # tensor-core K4 shapes: pages of 16 (8-page groups), GQA 1 and 2, a
+    # piece-mode split (b x kv_heads < SMs without cluster mode under CHESS_ATTN_TC=2)
+    (128, 32, 8, 16, 4, [1, 9, 30, 64], [16, 3, 9, 1]),
+    (128, 8, 8, 32, 18, [3, 4, 7, 12, 40, 2] * 3, [5, 32, 16, 17, 2, 31] * 3),
+    (128, 16, 8, 32, 6, [11, 1, 23, 4, 64, 6], [13, 7, 32, 30, 15, 1]),
 ]
 
 
@@ -168,6 +175,23 @@ def test_sparse_decode_vs_fp64(case):
         tol = attn_ref.bf16_bound(q[:, l].double().cpu().numpy(), kp[l], vp[l], bt, ws_lens, fills, scale, o_ref)
         assert np.all(np.abs(o - o_ref) <= tol), np.max(np.abs(o - o_ref) / tol)
         np.testing.assert_allclose(lse[l].double().cpu().numpy(), lse_ref, rtol=0, atol=2e-4)
+
+
+@pytest.mark.skipif(os.environ.get("CHESS_ATTN_TC") is not None, reason="already an alternate path")
+@pytest.mark.parametrize("tc", ["1", "2"], ids=["tcgen05_piece_streamk", "tcgen05_everywhere"])
+def test_attention_paths_in_subprocess(tc):
+    """K4 has two consumers: mma.sync (default) and tcgen05 (k_attn_tc.cuh,
+    head_dim 128, opt-in: CHESS_ATTN_TC=1 where cluster mode is not chosen, 2
+    everywhere).  Re-run the attention parity cases with the tensor-core one."""
+    import subprocess
+    import sys
+
+    here = os.path.dirname(os.path.abspath(__file__))
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider",
+                        os.path.join(here, "test_gpu_kernels.py"), "-k", "sparse_decode_vs_fp64"],
+                       env=dict(os.environ, CHESS_ATTN_TC=tc), capture_output=True, text=True,
+                       cwd=os.path.dirname(here), timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
 
 
 def test_entropy_logits_and_trigger_bitwise_stats():

@@ -49,7 +49,7 @@ struct Args {
   const __nv_bfloat16* P;  // [128 tok][8]
   float* S;                // [128][8]
   float* O;                // [128 d][8]
-  int form;                // 0: QK; 1: PV (P interleave); 2: PV (P K-major SW128)
+  int form;                // 0: QK; 1: PV (P interleave); 2: PV (P K-major SW128); 3: QK with M = 64
   uint32_t lbo_a, sbo_a, lbo_b, sbo_b;
 };
 
@@ -62,7 +62,16 @@ __global__ void __launch_bounds__(128) probe(Args a) {
   __shared__ uint32_t tm;
   const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
   // stage operands
-  if (a.form == 0) {
+  if (a.form == 3) {
+    for (int i = t; i < 64 * 16; i += 128) {  // K rows 0..63: [cb][64 rows][128 B]
+      const int r = i / 16, c = i % 16, cb = c / 8;
+      *reinterpret_cast<uint4*>(A + cb * 8192 + sw(r, c & 7)) = *reinterpret_cast<const uint4*>(a.K + r * 128 + c * 8);
+    }
+    for (int i = t; i < 8 * 16; i += 128) {
+      const int r = i / 16, c = i % 16, cb = c / 8;
+      *reinterpret_cast<uint4*>(Bq + cb * 1024 + sw(r, c & 7)) = *reinterpret_cast<const uint4*>(a.q + r * 128 + c * 8);
+    }
+  } else if (a.form == 0) {
     for (int i = t; i < 128 * 16; i += 128) {  // K: row r, chunk c (16 chunks of 8 elems)
       const int r = i / 16, c = i % 16, cb = c / 8;
       *reinterpret_cast<uint4*>(A + cb * 16384 + sw(r, c & 7)) = *reinterpret_cast<const uint4*>(a.K + r * 128 + c * 8);
@@ -102,7 +111,14 @@ __global__ void __launch_bounds__(128) probe(Args a) {
   const uint32_t tmem = tm;
   if (t == 0) {
     const uint32_t sa = su32(A), sb = su32(Bq);
-    if (a.form == 0) {
+    if (a.form == 3) {
+      const uint32_t id = idesc(64, 8, 0, 0);
+      for (int ks = 0; ks < 8; ++ks) {
+        const uint32_t off = (ks / 4) * 8192 + (ks % 4) * 32;
+        const uint32_t offb = (ks / 4) * 1024 + (ks % 4) * 32;
+        tc::mma_f16_ss(tmem, desc(sa + off, 16, 1024, 2), desc(sb + offb, 16, 1024, 2), id, ks != 0);
+      }
+    } else if (a.form == 0) {
       const uint32_t id = idesc(128, 8, 0, 0);
       for (int ks = 0; ks < 8; ++ks) {
         const uint32_t off = (ks / 4) * 16384 + (ks % 4) * 32;
@@ -135,18 +151,66 @@ __global__ void __launch_bounds__(128) probe(Args a) {
   }
   tc::fence_after();
   uint32_t r[8];
-  const uint32_t ta = tmem + ((uint32_t)(32 * warp) << 16) + (a.form == 0 ? 0u : 8u);
+  const uint32_t ta = tmem + ((uint32_t)(32 * warp) << 16) + ((a.form == 0 || a.form == 3) ? 0u : 8u);
   asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
                : "r"(ta));
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-  float* out = a.form == 0 ? a.S : a.O;
+  float* out = (a.form == 0 || a.form == 3) ? a.S : a.O;
   for (int j = 0; j < 8; ++j) out[t * 8 + j] = __uint_as_float(r[j]);
   tc::fence_before();
   __syncthreads();
   if (warp == 0) {
     tc::fence_after();
     tc::tmem_dealloc<32>(tmem);
+  }
+}
+
+// MMA latency: `reps` rounds of {8 MMAs (M128 N8 K16) into `nacc` accumulators, commit, wait}
+__global__ void __launch_bounds__(128) mma_latency(int nacc, int reps, long long* cycles, int nmma = 8, int slot = -1, int N = 8, int M = 128) {
+  extern __shared__ uint8_t raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(raw) + 1023) & ~uintptr_t(1023));
+  __shared__ uint64_t bar;
+  __shared__ uint32_t tm;
+  const int t = threadIdx.x, warp = t >> 5;
+  for (int i = t; i < 65536 / 16; i += 128) reinterpret_cast<uint4*>(sm)[i] = make_uint4(0, 0, 0, 0);
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  if (warp == 0) tc::tmem_alloc<256>(&tm);
+  if (t == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&bar)));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tmem = tm;
+  if (t == 0) {
+    const uint32_t sa = su32(sm), sb = su32(sm + 32768);
+    const uint32_t id = idesc(M, N, 0, 0);
+    long long t0 = clock64();
+    for (int r = 0; r < reps; ++r) {
+      for (int ks = 0; ks < nmma; ++ks) {
+        const int acc = ks % nacc;
+        const uint32_t off = ((ks / 4) & 1) * 16384 + (ks % 4) * 32;
+        tc::mma_f16_ss(tmem + acc * 8, desc(sa + off, 16, 1024, 2), desc(sb + ((ks / 4) & 1) * 1024 + (ks % 4) * 32, 16, 1024, 2), id, ks >= nacc);
+      }
+      tc::commit(&bar);
+      uint32_t done = 0;
+      while (!done) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(done)
+            : "r"(su32(&bar)), "r"(r & 1)
+            : "memory");
+      }
+    }
+    cycles[slot >= 0 ? slot : nacc] = (clock64() - t0) / reps;
+  }
+  tc::fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc::fence_after();
+    tc::tmem_dealloc<256>(tmem);
   }
 }
 
@@ -200,6 +264,52 @@ int main() {
       {"PV  A:MN SW128 lbo=1K sbo=16K  B:K-major SW128", 2, 1024, 16384, 16, 1024},
   };
   int ok_all = 1;
+  {
+    long long* dc;
+    cudaMalloc(&dc, 16 * 8);
+    cudaFuncSetAttribute(mma_latency, cudaFuncAttributeMaxDynamicSharedMemorySize, 80 * 1024);
+    for (int nacc : {1, 2, 4, 8}) mma_latency<<<1, 128, 80 * 1024>>>(nacc, 200, dc);
+    cudaDeviceSynchronize();
+    long long hc[16];
+    cudaMemcpy(hc, dc, 16 * 8, cudaMemcpyDeviceToHost);
+    printf("MMA round trip (8 x M128N8K16 + commit + wait), cycles: 1 acc %lld, 2 acc %lld, 4 acc %lld, 8 acc %lld\n",
+           hc[1], hc[2], hc[4], hc[8]);
+    int ns[6] = {1, 2, 4, 8, 16, 32};
+    for (int i = 0; i < 6; ++i) mma_latency<<<1, 128, 80 * 1024>>>(1, 200, dc, ns[i], i, 8);
+    cudaDeviceSynchronize();
+    cudaMemcpy(hc, dc, 16 * 8, cudaMemcpyDeviceToHost);
+    printf("N=8 round trip vs MMAs per round: 1: %lld 2: %lld 4: %lld 8: %lld 16: %lld 32: %lld\n", hc[0], hc[1], hc[2], hc[3], hc[4], hc[5]);
+    for (int i = 0; i < 6; ++i) mma_latency<<<1, 128, 80 * 1024>>>(1, 200, dc, ns[i], i, 32);
+    cudaDeviceSynchronize();
+    cudaMemcpy(hc, dc, 16 * 8, cudaMemcpyDeviceToHost);
+    printf("N=32 round trip vs MMAs per round: 1: %lld 2: %lld 4: %lld 8: %lld 16: %lld 32: %lld\n", hc[0], hc[1], hc[2], hc[3], hc[4], hc[5]);
+    int nn[6] = {8, 16, 64, 128, 256, 0};
+    for (int i = 0; i < 5; ++i) mma_latency<<<1, 128, 80 * 1024>>>(1, 200, dc, 16, i, nn[i], 128);
+    mma_latency<<<1, 128, 80 * 1024>>>(1, 200, dc, 16, 5, 8, 64);
+    cudaDeviceSynchronize();
+    cudaMemcpy(hc, dc, 16 * 8, cudaMemcpyDeviceToHost);
+    printf("16 MMAs M=128 by N: 8: %lld 16: %lld 64: %lld 128: %lld 256: %lld | M=64 N=8: %lld\n", hc[0], hc[1], hc[2], hc[3], hc[4], hc[5]);
+  }
+  {
+    // M = 64: where does row i of S land in TMEM (lane, column)?
+    Args a{dK, dq, dV, dP, dS, dO, 3, 16, 1024, 16, 1024};
+    cudaMemset(dS, 0, 128 * 8 * 4);
+    probe<<<1, 128, 40 * 1024>>>(a);
+    if (cudaDeviceSynchronize() != cudaSuccess) { printf("M=64 probe failed\n"); return 1; }
+    std::vector<float> got(128 * 8);
+    cudaMemcpy(got.data(), dS, 128 * 8 * 4, cudaMemcpyDeviceToHost);
+    printf("M=64 QK: TMEM lane of S row i (col 0) [first 64 rows]:");
+    int okm = 1;
+    for (int i = 0; i < 64; ++i) {
+      int where = -1;
+      for (int ln = 0; ln < 128; ++ln)
+        if (fabs(got[ln * 8] - Sref[i * 8]) <= 1e-3 * (1 + fabs(Sref[i * 8]))) { where = ln; break; }
+      printf(" %d", where);
+      if (where >= 0) for (int h = 0; h < 8; ++h) okm &= fabs(got[where * 8 + h] - Sref[i * 8 + h]) <= 1e-3 * (1 + fabs(Sref[i * 8 + h]));
+      else okm = 0;
+    }
+    printf("\nM=64 QK rows found with all 8 columns in one lane: %s\n", okm ? "yes" : "no");
+  }
   for (auto& v : vs) {
     Args a{dK, dq, dV, dP, dS, dO, v.form, v.la, v.sa, v.lb, v.sb};
     cudaMemset(dS, 0, 128 * 8 * 4);
