@@ -165,7 +165,7 @@ struct Cfg {
   static constexpr int kPK = B / 16;                   // PV k-steps (16 tokens each)
   static constexpr int kEPL = GQ * HD / 32;            // merge: state elements per lane
   static constexpr size_t kSmem = 1024 + (size_t)kStages * kStageBytes + kStateBytes +
-                                  kQSlots * kQBytes + kXBytes + (2 * kStages + 2 * kQSlots + 1) * 8 +
+                                  kQSlots * kQBytes + kXBytes + (2 * kStages + 2 * kQSlots + 3) * 8 +
                                   64 + kTables;
   static_assert(kStages >= 4, "ring too shallow");
   static_assert(GQ <= 8, "one GQA group per n8 tile");
@@ -245,13 +245,18 @@ __device__ __forceinline__ void consumer_sync() {
   asm volatile("bar.sync 2, %0;" ::"n"(kConsumers * 32) : "memory");
 }
 
+// The producer's "pages issued" counter: atomic acquire / release on shared
+// memory (an atomic is never a data race, so compute-sanitizer racecheck has
+// nothing to report on the handoff).
 __device__ __forceinline__ int ld_acquire_cta(const int* p) {
   int v;
-  asm volatile("ld.acquire.cta.shared::cta.b32 %0, [%1];" : "=r"(v) : "r"(smem_u32(p)) : "memory");
+  asm volatile("atom.acquire.cta.shared::cta.or.b32 %0, [%1], 0;" : "=r"(v) : "r"(smem_u32(p)) : "memory");
   return v;
 }
 __device__ __forceinline__ void st_release_cta(int* p, int v) {
-  asm volatile("st.release.cta.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(p)), "r"(v) : "memory");
+  int old;
+  asm volatile("atom.release.cta.shared::cta.exch.b32 %0, [%1], %2;" : "=r"(old) : "r"(smem_u32(p)), "r"(v) : "memory");
+  (void)old;
 }
 
 // Consumer math layout ("tokens as M"): per page, S^T = K q^T with the
@@ -298,7 +303,9 @@ __global__ void __launch_bounds__(kThreads, CPS)
   uint64_t* qfull = empty + C::kStages;
   uint64_t* qempty = qfull + C::kQSlots;
   uint64_t* xbar = qempty + C::kQSlots;                    // leader's inbox barrier (XC)
-  int* ctr = reinterpret_cast<int*>(xbar + 1);             // [0] issued, [1] st_cnt, [2] st_next
+  uint64_t* stbar = xbar + 1;                               // piece states written (kConsumers arrivals)
+  uint64_t* slotfree = stbar + 1;                            // piece states read by the merger (1 arrival)
+  int* ctr = reinterpret_cast<int*>(slotfree + 1);           // [0] issued, [1] st_cnt
   int* prefix = ctr + 16;                                   // [nb + 1] pages before slot s
   int* s_np = prefix + kAttnMaxBatch + 1;                   // [nb] pages per segment of slot s
   int* s_fill = s_np + kAttnMaxBatch;                        // [nb] valid rows of the last page
@@ -396,8 +403,9 @@ __global__ void __launch_bounds__(kThreads, CPS)
       mbar_arrive_expect_tx(xbar, (uint32_t)(args.cl - 1) * (uint32_t)(GQ * (HD + 2) * 4));
     }
     ctr[0] = 0;
+    mbar_init(stbar, kConsumers * 32);
+    mbar_init(slotfree, 32);
     ctr[1] = 0;
-    ctr[2] = 0;
     fence_barrier_init();
   }
   __syncthreads();
@@ -715,11 +723,8 @@ __global__ void __launch_bounds__(kThreads, CPS)
     if (k == 0 && args.mode != 8) pdl_wait();
     if (k == 0 && lane == 0) trace_max(5);  // debug timeline: last warp past the PDL wait
     const long long ck0 = kTrace ? clock64() : 0;
-    if (lane == 0) {
-      while (ld_acquire_cta(&ctr[2]) != k) {
-      }
-    }
-    __syncwarp();
+    // the state slots are free once the previous piece's merger read them
+    if (k > 0) mbar_wait(slotfree, (uint32_t)((k - 1) & 1));
     const long long ck1 = kTrace ? clock64() : 0;
 #pragma unroll
     for (int e = 0; e < 2; ++e) {
@@ -805,21 +810,19 @@ __global__ void __launch_bounds__(kThreads, CPS)
       ++k;
       continue;
     }
+    // Piece-state handoff: every warp arrives on stbar (release) after its
+    // state stores; the last to arrive (shared counter) merges after waiting
+    // on stbar (acquire) and frees the slots through slotfree.  mbarrier
+    // phases make the ordering explicit (compute-sanitizer racecheck models
+    // them; the earlier fence + atomic handoff it could not see).
     int last = 0;
-    if (lane == 0) {
-      __threadfence_block();
-      last = atomicAdd(&ctr[1], 1) == kConsumers - 1;
-    }
+    mbar_arrive(stbar);  // every lane: its own state stores are released
+    if (lane == 0) last = atomicAdd(&ctr[1], 1) == kConsumers - 1;
     last = __shfl_sync(0xffffffffu, last, 0);
     const long long ck2 = kTrace ? clock64() : 0;
     if (last) {
       // ---- this warp merges the piece (warp order, deterministic) ----
-      // writers: lanes' stores -> __syncwarp -> lane 0 fence.cta + atomic;
-      // reader: lane 0 atomic -> fence.cta -> __syncwarp -> lanes' loads.
-      // (compute-sanitizer racecheck models barriers, not fence+atomic
-      // handoffs, and reports this exchange as a hazard.)
-      __threadfence_block();
-      __syncwarp();
+      mbar_wait(stbar, (uint32_t)(k & 1));
       const int hh = (lane * C::kEPL) / HD, el = (lane * C::kEPL) % HD;
       float M = -INFINITY, L = 0.f, acc[C::kEPL];
 #pragma unroll
@@ -850,11 +853,8 @@ __global__ void __launch_bounds__(kThreads, CPS)
         }
       }
       // the slot is free again once the states are in registers
-      __syncwarp();
-      if (lane == 0) {
-        ctr[1] = 0;
-        st_release_cta(&ctr[2], k + 1);
-      }
+      if (lane == 0) atomicExch(&ctr[1], 0);
+      mbar_arrive(slotfree);  // every lane of the merger: its reads are done
       if (lane == 0) trace_max(6);
       const long long ck3 = kTrace ? clock64() : 0;
       if (kTrace && lane == 0) {
