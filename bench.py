@@ -485,7 +485,8 @@ def run_gpu(args):
             "unique_tiles_per_launch": k4_unique_tiles,
         },
         "select_roofline": {
-            "kernel": "select cascade (K2+K3, 3 launches)",
+            "kernel": ("select cascade: anchor split + per level tcgen05 fp16 scan + exact f64 rescoring (7 launches)"
+                       if args.summary_dtype == "f16tc" else "select cascade (K2+K3, 3 launches)"),
             "achieved": sel_call_bytes / select_call_s / 1e9,
             "peak": hbm_peak, "unit": "GB/s",
             "frac": sel_call_bytes / select_call_s / 1e9 / hbm_peak,
