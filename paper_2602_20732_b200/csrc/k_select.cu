@@ -1508,8 +1508,10 @@ static int launch_select_tc(const ChessState& st, const Workspace& ws, const Sel
   }
   SelParams pr = prm;
   pr.rescore = 1;
+  static const int grid_override = getenv("CHESS_SELECT_GRID") ? atoi(getenv("CHESS_SELECT_GRID")) : 0;  // A/B
+  const int grid = grid_override > 0 ? grid_override : num_sms();
   for (int level = 0; level < 3; ++level) {
-    select_tc_kernel<<<num_sms(), kTcCTA, tc_smem(d.batch), stream>>>(st, ws, prm, level, mg, mc, mp);
+    select_tc_kernel<<<grid, kTcCTA, tc_smem(d.batch), stream>>>(st, ws, prm, level, mg, mc, mp);
     if ((rc = check_launch("select_tc"))) return rc;
     if ((rc = launch_scan<double>(st, ws, pr, level, stream))) return rc;
   }

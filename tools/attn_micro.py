@@ -80,8 +80,10 @@ def main():
         with torch.cuda.graph(graph, stream=gs):
             for r in range(per_graph):
                 for layer in range(L):
-                    _lib.call("chess_sparse_decode", st.ref, layer, _lib.ptr(q[:, layer]), q.stride(0),
-                              _lib.ptr(out[:, layer]), out.stride(0), None, 0.088, _lib.stream_ptr(gs))
+                    # as the engine: every layer after the first follows another K4
+                    _lib.call("chess_sparse_decode_ex", st.ref, layer, _lib.ptr(q[:, layer]), q.stride(0),
+                              _lib.ptr(out[:, layer]), out.stride(0), None, 0.088,
+                              _lib.ATTN_AFTER_DECODE if (r or layer) else 0, _lib.stream_ptr(gs))
         torch.cuda.current_stream().wait_stream(gs)
         graph.replay()
         torch.cuda.synchronize()
