@@ -105,6 +105,48 @@ def _ncu_traffic(cfg_name, kernel):
         return None
 
 
+def _shard_plan(args, world):
+    """(shard, batch per rank, sequences the job advances per step, cfg) for
+    --config / --shard / --batch at `world` ranks: cfg4 splits
+    its batch across ranks, cfg5 its KV heads; other configs run one replica
+    per rank (weak scaling)."""
+    from paper_2602_20732_b200.synthetic import CONFIGS
+
+    c = dict(CONFIGS[args.config])
+    if args.page_size:
+        c["page"] = args.page_size
+    batch = c["batch"] if args.batch is None else args.batch
+    shard = args.shard
+    if shard == "auto":
+        shard = {"cfg4": "batch", "cfg5": "head"}.get(args.config, "replica") if world > 1 else "replica"
+    if shard == "batch" and args.batch is None:
+        batch = max(1, c["batch"] // world)
+    job_batch = batch if shard == "head" else world * batch
+    return shard, batch, job_batch, c
+
+
+def workload_config(args, world):
+    """The JSON line's `config`: the workload both arms run (the chess arm's
+    run-specific details go to `details`), so the two lines compare equal."""
+    from paper_2602_20732_b200.synthetic import DESCRIPTIONS
+
+    shard, batch, job_batch, c = _shard_plan(args, world)
+    return {
+        "workload": f"{args.config}: {DESCRIPTIONS[args.config]}",
+        "batch_per_gpu": batch,
+        "batch_total": job_batch,
+        "context": c["ctx"],
+        "page_size": c["page"],
+        "preset": "aggressive (0.5, 0.2, 0.1), W=4, sinks=1",
+        "parallelism": ("single GPU" if world == 1 and shard == "replica" else
+                        {"batch": f"batch-shard x{world} (no data-path collective)",
+                         "head": f"kv-head-shard x{world} (per-level partial-score exchange and per-layer output "
+                                 "gather: " + ("peer-memory stores fused into the producing kernels"
+                                               if args.transport == "p2p" else "NCCL all-gather") + ")",
+                         "replica": f"replicas x{world} (no data-path collective)"}[shard]),
+    }
+
+
 # ---------------------------------------------------------------------------
 # GPU arm
 # ---------------------------------------------------------------------------
@@ -141,17 +183,7 @@ def run_gpu(args):
     peak_src = "measured" if "hbm_gbs" in peaks else "fallback"
 
     cfg_name = args.config
-    c = dict(CONFIGS[cfg_name])
-    if args.page_size:
-        c["page"] = args.page_size
-    batch = c["batch"] if args.batch is None else args.batch
-    # sharding: cfg4 splits its batch across ranks, cfg5 its KV
-    # heads; other configs run one replica per rank (weak scaling)
-    shard = args.shard
-    if shard == "auto":
-        shard = {"cfg4": "batch", "cfg5": "head"}.get(cfg_name, "replica") if world > 1 else "replica"
-    if shard == "batch" and args.batch is None:
-        batch = max(1, c["batch"] // world)
+    shard, batch, job_batch, c = _shard_plan(args, world)
     head = shard == "head"
     ring = 64 if c["page"] == 32 else 32
     # variants (dynamic, attention-only) run at least two rings so their
@@ -181,8 +213,6 @@ def run_gpu(args):
                         torch.device("cuda", local), full_scan=args.full_scan)
         if args.transport == "p2p":
             exchange.connect()  # IPC handles over the default group
-    # sequences the whole job advances per step
-    job_batch = batch if head else world * batch
 
     def fresh_decoder(policy, thresholds=None):
         st.reset()
@@ -444,20 +474,8 @@ def run_gpu(args):
         "vs_baseline": None,
         "dtype": DTYPES[args.summary_dtype],
         "data": "synthetic (planted-relevance keys, random-init shapes)",
-        "config": {
-            "workload": f"{cfg_name}: {DESCRIPTIONS[cfg_name]}",
-            "batch_per_gpu": batch,
-            "context": c["ctx"],
-            "page_size": B,
-            "preset": "aggressive (0.5, 0.2, 0.1), W=4, sinks=1",
-            "parallelism": ("single GPU" if world == 1 and shard == "replica" else
-                            {"batch": f"batch-shard x{world} (no data-path collective)",
-                             "head": f"kv-head-shard x{world} (per-level partial-score exchange: "
-                                     + ("peer-memory stores fused into the scan tail"
-                                        if args.transport == "p2p" else "NCCL all-gather")
-                                     + "; per-layer output all-gather: NCCL)",
-                             "replica": f"replicas x{world} (no data-path collective)"}[shard]),
-            "batch_total": job_batch,
+        "config": workload_config(args, world),
+        "details": {
             "summary_dtype": args.summary_dtype,
             "scan": "full (Alg.1 literal)" if args.full_scan else "conditional (output-identical)",
             "kv_pool_pages": sh.n_phys,
@@ -622,7 +640,7 @@ def run_reference(args):
         "value": v, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"{args.config}: {DESCRIPTIONS[args.config]}"},
+        "config": workload_config(args, world),
         "cpu_baseline": {"value": v, "unit": "tokens/s", "cores": cores, "kind": "port",
                          "sample": sample},
         "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},

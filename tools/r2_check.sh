@@ -8,5 +8,5 @@ tail -3 gpurun_out/r2c/bench_20_5.err
 for f in gpurun_out/r2c/bench_*.json; do python -c "
 import sys,json
 d=json.loads(open('$f').read().strip().splitlines()[-1])
-r=d['roofline']; print('$f', round(d['us_per_step'],1), round(r['launch_us'],2), round(r['frac'],3), r.get('tiles_per_launch'), r.get('unique_tiles_per_launch'), round(d['config']['ws_pages_mean'],2), round(d['select_roofline']['call_us'],1), json.dumps(d.get('variants')))
+r=d['roofline']; print('$f', round(d['us_per_step'],1), round(r['launch_us'],2), round(r['frac'],3), r.get('tiles_per_launch'), r.get('unique_tiles_per_launch'), round(d['details']['ws_pages_mean'],2), round(d['select_roofline']['call_us'],1), json.dumps(d.get('variants')))
 "; done

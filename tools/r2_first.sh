@@ -11,5 +11,5 @@ import sys,json
 for l in sys.stdin:
     l=l.strip()
     if l.startswith('{'):
-        d=json.loads(l); print(d['us_per_step'], d['roofline']['launch_us'], d['roofline']['bytes_per_launch'], d['config']['kv_pool_pages'], d['config']['ws_pages_mean'], d['select_roofline']['call_us'])
+        d=json.loads(l); print(d['us_per_step'], d['roofline']['launch_us'], d['roofline']['bytes_per_launch'], d['details']['kv_pool_pages'], d['details']['ws_pages_mean'], d['select_roofline']['call_us'])
 "
