@@ -684,6 +684,13 @@ def run_plumbing(args):
         dist.destroy_process_group()
 
 
+# --summary-dtype auto: the measured-faster selection path per config
+# (profiles/r02/dtype_sweep/summary.txt, one box): the tensor-core scan halves
+# the selection's bytes but runs 7 launches with 6 per-slot tails instead of 3;
+# only at cfg3 (16 x 4096 pages of 32768-wide rows) do the bytes win
+# (787 vs 873 us/step); at cfg1/cfg2/cfg4/cfg5 f32 mirrors are faster.
+AUTO_DTYPE = {"cfg3": "f16tc"}
+
 DTYPES = {
     "f16tc": "bf16 KV / fp16 summary mirrors on tcgen05 (certified bounds) + exact f64 rescoring near each cut",
     "f32": "bf16 KV / f32 summary mirrors / f64 scores",
@@ -701,9 +708,11 @@ def main():
     ap.add_argument("--impl", default="chess", choices=["chess", "reference"])
     ap.add_argument("--config", default="cfg3")
     ap.add_argument("--batch", type=int, default=None)
-    ap.add_argument("--summary-dtype", default="f16tc", choices=["f32", "f64", "bf16", "f16tc"],
-                    help="f16tc (default): fp16 mirrors scored on tcgen05 with certified bounds, exact f64 "
-                         "rescoring near each cut (selections identical to the f64 scores)")
+    ap.add_argument("--summary-dtype", default="auto", choices=["auto", "f32", "f64", "bf16", "f16tc"],
+                    help="f16tc: fp16 mirrors scored on tcgen05 with certified bounds, exact f64 rescoring "
+                         "near each cut (selections identical to the f64 scores); f32: f32 mirrors on CUDA "
+                         "cores.  auto (default): the faster of the two per config, measured "
+                         "(profiles/r02/dtype_sweep/summary.txt): f16tc at cfg3, f32 elsewhere")
     ap.add_argument("--full-scan", action="store_true")
     ap.add_argument("--headline-only", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -715,6 +724,8 @@ def main():
     ap.add_argument("--shard", default="auto", choices=["auto", "batch", "head", "replica"],
                     help="multi-GPU partitioning (auto: cfg4 batch, cfg5 kv-head, else replicas)")
     args = ap.parse_args()
+    if args.summary_dtype == "auto":
+        args.summary_dtype = AUTO_DTYPE.get(args.config, "f32")
     if args.warmup < 3:
         args.warmup = 3
     env_world = os.environ.get("WORLD_SIZE")
