@@ -732,6 +732,7 @@ __global__ void __launch_bounds__(kScanCTA, CHESS_SCAN_MINB) select_scan_kernel(
 // on items of its own level, which never wait on later levels.
 // ---------------------------------------------------------------------------
 constexpr int kSmallRowBytes = 16384;  // rows up to this size use select_small_kernel
+constexpr int kSmallCand = 1024;       // select_small_kernel: candidates per level kept in shared memory
 constexpr int kDescRing = 8;
 constexpr int kFlowMaxBatch = 256;  // per-slot scheduler tables live in shared memory
 constexpr int kDescEnd = -1, kDescFlush = -2;
@@ -1110,42 +1111,113 @@ __global__ void __launch_bounds__(kNT) select_small_kernel(ChessState st, Worksp
     return;
   }
   // the anchor once into shared memory (rows here are <= 16 KB: <= 4096
-  // elements of f32 / 2048 of f64)
-  __shared__ double s_anc[kSmallRowBytes / 4];
+  // elements of f32 / 2048 of f64; dynamic shared memory, d.dim doubles)
+  extern __shared__ double s_anc[];
   const double* anc_g = st.anchor + (int64_t)s * d.ld;
   for (int j = threadIdx.x; j < d.dim; j += kNT) s_anc[j] = anc_g[j];
   block_sync<kNT>();
-  double* sc = ws.scores + (int64_t)s * max_rows(d);
-  for (int level = 0; level < 3; ++level) {
-    const int n = level == 0 ? sh.G : ws.cand_n[4 * s + level];
-    for (int i = warp; i < n; i += kNT / 32) {
-      const T* row = level_row_ptr<T>(st, ws, s, level, i, sh);
-      double acc = 0.0;
-      // Same order as a plain j = lane, lane + 32, ... FMA chain (exact f64
-      // parity, signed zeros included), but the row loads of 16 steps are
-      // issued before their FMAs: one memory latency per 512 elements
-      // instead of one per 32 (cfg1 pass 45 us of latency under ncu).
-      for (int j0 = lane; j0 < d.dim; j0 += 32 * 16) {
-        using V = decltype(to_f(row[0]));  // f32 (f32 / bf16 mirrors) or f64 rows
-        V r[16];
+  const int64_t mr = max_rows(d);
+  double* sc = ws.scores + (int64_t)s * mr;
+  // dot product of one summary row with the anchor by one warp: the plain
+  // j = lane, lane + 32, ... FMA chain (exact f64 parity, signed zeros
+  // included), with the row loads of 16 steps issued before their FMAs (one
+  // memory latency per 512 elements instead of one per 32)
+  auto dot = [&](const T* row) {
+    double acc = 0.0;
+    for (int j0 = lane; j0 < d.dim; j0 += 32 * 16) {
+      using V = decltype(to_f(row[0]));  // f32 (f32 / bf16 mirrors) or f64 rows
+      V r[16];
 #pragma unroll
-        for (int k = 0; k < 16; ++k) {
-          const int j = j0 + 32 * k;
-          r[k] = j < d.dim ? to_f(row[j]) : V(0);
-        }
-#pragma unroll
-        for (int k = 0; k < 16; ++k) {
-          const int j = j0 + 32 * k;
-          if (j < d.dim) acc = __fma_rn(s_anc[j], (double)r[k], acc);
-        }
+      for (int k = 0; k < 16; ++k) {
+        const int j = j0 + 32 * k;
+        r[k] = j < d.dim ? to_f(row[j]) : V(0);
       }
 #pragma unroll
-      for (int o = 16; o >= 1; o >>= 1) acc += shfl_xor_d(acc, o);
-      if (lane == 0) sc[i] = acc;
+      for (int k = 0; k < 16; ++k) {
+        const int j = j0 + 32 * k;
+        if (j < d.dim) acc = __fma_rn(s_anc[j], (double)r[k], acc);
+      }
+    }
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) acc += shfl_xor_d(acc, o);
+    return acc;
+  };
+  if (sh.G > kTailCap || sh.C > kSmallCand || sh.P > kSmallCand) {
+    // large index: the shared tail (candidates and scores in global memory)
+    for (int level = 0; level < 3; ++level) {
+      const int n = level == 0 ? sh.G : ws.cand_n[4 * s + level];
+      for (int i = warp; i < n; i += kNT / 32) {
+        const double acc = dot(level_row_ptr<T>(st, ws, s, level, i, sh));
+        if (lane == 0) sc[i] = acc;
+      }
+      block_sync<kNT>();
+      select_tail_topk(st, ws, prm, s, level, n, sm);
+      block_sync<kNT>();
+    }
+    return;
+  }
+  // Every level's candidates, keys and kept parents stay in shared memory:
+  // the global round trips of the shared tail (scores written and read back,
+  // candidate counts, candidate ids behind each row pointer) were most of a
+  // cfg1 pass.  Global candidate lists / counts / scores are still written
+  // (write-only) for the debug readers.
+  __shared__ int s_cand[kSmallCand];
+  __shared__ int s_plist[kSmallCand];
+  __shared__ int s_cnt;
+  int* stats = st.sel_stats + 8 * s;
+  int m = sh.G;
+  for (int lv = 0; lv < 3; ++lv) {
+    // rows of this level (level_row_ptr's layout: f64 rows in *_vec64, f32 /
+    // bf16 mirrors in the *_vec32 buffers)
+    const void* b64 = lv == 0 ? (const void*)st.grid_vec64 : (lv == 1 ? (const void*)st.chunk_vec64 : (const void*)st.page_vec64);
+    const void* b32 = lv == 0 ? (const void*)st.grid_vec32 : (lv == 1 ? (const void*)st.chunk_vec32 : (const void*)st.page_vec32);
+    const int64_t lrows = lv == 0 ? max_grids(d) : (lv == 1 ? max_chunks(d) : (int64_t)d.max_pages);
+    const T* base = reinterpret_cast<const T*>(sizeof(T) == 8 ? b64 : b32) + (int64_t)s * lrows * d.ld;
+    for (int i = warp; i < m; i += kNT / 32) {
+      const int id = lv == 0 ? i : s_cand[i];
+      const double acc = dot(base + (int64_t)id * d.ld);
+      if (lane == 0) {
+        sm.keys[i] = score_key(acc);
+        sc[i] = acc;
+      }
     }
     block_sync<kNT>();
-    select_tail_topk(st, ws, prm, s, level, n, sm);
+    const int k = (int)ceil(prm.rho[lv] * (double)m);  // selection.py:98, 103, 108
+    block_topk_mark<kNT>(sm.keys, m, k, sm.kept, sm.hist, sm.scratch);
+    if (lv < 2) {
+      const int kcount = block_compact<kNT>(sm.kept, m, s_plist, sm.scratch,
+                                            [&](int i) { return lv == 0 ? i : s_cand[i]; });
+      block_sync<kNT>();
+      const int fan = lv == 0 ? d.chunks_per_grid : d.pages_per_chunk;
+      const int total_children = lv == 0 ? sh.C : sh.P;
+      expand_children(s_plist, kcount, fan, total_children, s_cand, &s_cnt);
+      block_sync<kNT>();
+      m = s_cnt;
+      int* gc = ws.cand + ((int64_t)s * 3 + lv + 1) * mr;
+      for (int i = threadIdx.x; i < m; i += kNT) gc[i] = s_cand[i];
+      if (threadIdx.x == 0) {
+        ws.cand_n[4 * s + lv + 1] = m;
+        stats[5 + lv] = kcount;
+        stats[3 + lv] = m;
+      }
+    } else {
+      int32_t* sem = st.semantic + (int64_t)s * d.max_pages;
+      const int kcount = block_compact<kNT>(sm.kept, m, sem, sm.scratch, [&](int i) { return s_cand[i]; });
+      if (threadIdx.x == 0) {
+        st.n_semantic[s] = kcount;
+        stats[7] = kcount;
+        stats[0] = sh.G;
+        stats[1] = sh.C;
+        stats[2] = sh.P;
+      }
+    }
     block_sync<kNT>();
+  }
+  __threadfence_block();
+  if (prm.defer_ws) {  // the block table is being read by a concurrent decode
+    if (threadIdx.x == 0) ws.ws_pending[s] = 1;
+  } else {
+    block_build_ws<kNT>(st, s, sm.scratch);
   }
 }
 
@@ -1579,12 +1651,22 @@ int launch_select(const ChessState& st, const Workspace& ws, const SelParams& pr
   static const int small_env = getenv("CHESS_SELECT_SMALL") ? atoi(getenv("CHESS_SELECT_SMALL")) : 1;
   if (small_env && !prm.full_scan && !prm.xout && !prm.xpeer && prm.mode == 0 &&
       st.d.ld * summary_elem_bytes(st.d.summary_dtype) <= kSmallRowBytes) {
+    // dynamic shared memory: the slot's anchor (d.dim doubles, <= 32 KB)
+    const size_t dyn = (size_t)st.d.dim * sizeof(double);
+    static bool configured = false;
+    if (!configured) {
+      cudaFuncSetAttribute(select_small_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmallRowBytes * 2);
+      cudaFuncSetAttribute(select_small_kernel<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           kSmallRowBytes * 4);
+      cudaFuncSetAttribute(select_small_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmallRowBytes);
+      configured = true;
+    }
     if (st.d.summary_dtype == 0)
-      select_small_kernel<float><<<st.d.batch, kNT, 0, stream>>>(st, ws, prm);
+      select_small_kernel<float><<<st.d.batch, kNT, dyn, stream>>>(st, ws, prm);
     else if (st.d.summary_dtype == 2)
-      select_small_kernel<__nv_bfloat16><<<st.d.batch, kNT, 0, stream>>>(st, ws, prm);
+      select_small_kernel<__nv_bfloat16><<<st.d.batch, kNT, dyn, stream>>>(st, ws, prm);
     else
-      select_small_kernel<double><<<st.d.batch, kNT, 0, stream>>>(st, ws, prm);
+      select_small_kernel<double><<<st.d.batch, kNT, dyn, stream>>>(st, ws, prm);
     return check_launch("select_small");
   }
   const int nlev = prm.full_scan ? 1 : 3;

@@ -3,4 +3,4 @@ timeout 1500 python -m pytest tests/test_gpu_select.py tests/test_gpu_pagesel.py
 for cfg in cfg1; do timeout 300 python bench.py --config $cfg --steps 40 --warmup 5 --no-cpu-baseline --headline-only > gpurun_out/s3u/bench_$cfg.json 2>/dev/null; python -c "
 import json
 d=json.loads(open('gpurun_out/s3u/bench_$cfg.json').read().strip().splitlines()[-1])
-print('$cfg', round(d['us_per_step'],1), 'K4', round(d['roofline']['launch_us'],2), 'sel', round(d['select_roofline']['call_us'],1), d['variants'])"; done
+print('$cfg', round(d['us_per_step'],1), 'K4', round(d['roofline']['launch_us'],2), 'sel', round(d['select_roofline']['call_us'],1))"; done
