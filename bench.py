@@ -196,9 +196,13 @@ def run_gpu(args):
     pre_roll = 4 * c["page"]
     total_steps = pre_roll + args.warmup + max(args.steps, var_steps)
     gen_pages = math.ceil((total_steps + 2 * ring + 64) / c["page"]) + 4
+    kv_gib = args.kv_gib
+    if kv_gib is None and os.environ.get("CHESS_BENCH_ONE_DEVICE") == "1" and world > 1:
+        # plumbing mode: every rank shares cuda:0, so each takes a share of its memory
+        kv_gib = max(4.0, torch.cuda.mem_get_info(local)[0] / 2**30 * 0.6 / world - 8.0)
     wl = SyntheticDecode(cfg_name, batch=batch, gen_pages=gen_pages, ring=ring, seed=rank,
                          summary_dtype=args.summary_dtype, head_shard=(rank, world) if head else None,
-                         kv_budget_gib=args.kv_gib, page_size=args.page_size)
+                         kv_budget_gib=kv_gib, page_size=args.page_size)
     st = wl.st
     sh = wl.shape
     sel = preset_config("aggressive", page_size=sh.page_size)
