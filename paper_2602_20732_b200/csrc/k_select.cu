@@ -1509,7 +1509,7 @@ __global__ void gather_pages_kernel(const int32_t* table, int n_pages, const int
 // ---------------------------------------------------------------------------
 template <typename T>
 static int launch_scan(const ChessState& st, const Workspace& ws, const SelParams& prm, int level,
-                       cudaStream_t stream) {
+                       cudaStream_t stream, int grid_default = 0) {
   using SC = ScanCfg<T>;
   const size_t smem = 128 + (size_t)SC::kStages * SC::kStageBytes + 2 * SC::kStages * 8 +
                       (size_t)(2 * st.d.batch + 1) * sizeof(int);
@@ -1521,7 +1521,8 @@ static int launch_scan(const ChessState& st, const Workspace& ws, const SelParam
     configured = true;
   }
   static const int grid_override = getenv("CHESS_SELECT_GRID") ? atoi(getenv("CHESS_SELECT_GRID")) : 0;  // debug
-  select_scan_kernel<T><<<grid_override > 0 ? grid_override : num_sms(), kScanCTA, smem, stream>>>(st, ws, prm, level);
+  const int grid = grid_override > 0 ? grid_override : (grid_default > 0 ? grid_default : num_sms());
+  select_scan_kernel<T><<<grid, kScanCTA, smem, stream>>>(st, ws, prm, level);
   return check_launch("select_scan");
 }
 
@@ -1602,12 +1603,17 @@ static int launch_select_tc(const ChessState& st, const Workspace& ws, const Sel
   }
   SelParams pr = prm;
   pr.rescore = 1;
+  // Next to a concurrent decode (defer_ws: the engine's overlapped step) the
+  // scan and rescoring launches run on 96 of 148 CTAs: measured on the cfg3 step (two runs each,
+  // profiles/r02/select_grid_sweep.txt) 775.6 us at 96 against 791.1 at 148,
+  // 779-782 at 80-88 / 104-112 and 797 at 64-72; the pass alone is faster
+  // on every SM (328 vs 373 us), which is what a standalone selection gets.
   static const int grid_override = getenv("CHESS_SELECT_GRID") ? atoi(getenv("CHESS_SELECT_GRID")) : 0;  // A/B
-  const int grid = grid_override > 0 ? grid_override : num_sms();
+  const int grid = grid_override > 0 ? grid_override : (prm.defer_ws ? std::max(1, num_sms() * 96 / 148) : num_sms());
   for (int level = 0; level < 3; ++level) {
     select_tc_kernel<<<grid, kTcCTA, tc_smem(d.batch), stream>>>(st, ws, prm, level, mg, mc, mp);
     if ((rc = check_launch("select_tc"))) return rc;
-    if ((rc = launch_scan<double>(st, ws, pr, level, stream))) return rc;
+    if ((rc = launch_scan<double>(st, ws, pr, level, stream, grid))) return rc;
   }
   return CHESS_OK;
 }
