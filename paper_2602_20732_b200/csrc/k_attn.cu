@@ -92,6 +92,7 @@ struct AttnArgs {
   int layer;
   int cl;    // cluster-merge mode: CTAs per segment (= cluster size), 0 = off
   int prefetch;  // pages past the first run prefetched into L2 before the PDL wait
+  int next_pf;   // pages of the CTA's range prefetched into L2 for layer + 1 once its own loads are issued
   // Head-shard output gather over peer memory (chess_sparse_decode_gather):
   // every output row is also stored at the same offset from peer_out[p]
   // (this rank's block in peer p's region, NVLink stores).
@@ -552,6 +553,19 @@ __global__ void __launch_bounds__(kThreads, CPS)
       }
       cur_row = nxt_row;
       cur_tag = nxt_tag;
+    }
+    // Every layer's launch walks the same block table with the same work
+    // split, so this CTA's first pages are the next layer's first pages on the
+    // same position: once this layer's loads are all issued (the ring only
+    // drains from here), pull the next layer's first tiles into L2 so that
+    // layer's start hits L2 instead of HBM (an L2 hint: no data dependency).
+    if (args.next_pf > 0 && args.layer + 1 < d.layers && n > 0) {
+      int row0, tag;
+      fetch(0, row0, tag);
+      if (lane < min(args.next_pf, min(n, 32))) {
+        tma_prefetch_4d(&kmap, 0, row0, 0, args.layer + 1);
+        tma_prefetch_4d(&vmap, 0, row0, 0, args.layer + 1);
+      }
     }
     return;
   }
@@ -1170,6 +1184,13 @@ int launch_inst(const ChessState& st, const Workspace& ws, const AttnArgs& args_
   AttnArgs args = args_in;
   const int segs = st.d.batch * st.d.kv_heads;
   args.cl = args.mode == 7 ? 0 : cluster_size_for<HD, GQ, B>(segs);
+  // next-layer L2 prefetch (see the producer): piece mode only, where CTA c
+  // owns the same segment piece in every layer.  Measured (profiles/r02/
+  // k4_next_layer_prefetch.txt): cfg3 K4 18.18 -> 17.8 us, dynamic step
+  // 614.6 -> 602.8 us, headline neutral; stream-K (cfg4, two CTAs per SM)
+  // 47.5 -> 48.6 us and cluster mode (cfg2, cfg5) neutral or worse: off there.
+  static const int next_pf_env = getenv("CHESS_ATTN_NEXTPF") ? atoi(getenv("CHESS_ATTN_NEXTPF")) : -1;  // A/B
+  args.next_pf = next_pf_env >= 0 ? next_pf_env : (args.cl == 0 && segs <= num_sms() ? 8 : 0);
   // CHESS_ATTN_TC: 0 (default) mma.sync consumer; 1 tensor-core consumer
   // (k_attn_tc.cuh) wherever cluster mode is not chosen; 2 everywhere.
   // Measured on B200 (profiles/r02/k4_tc/): a tcgen05.mma of kind::f16 costs
@@ -1256,6 +1277,7 @@ int launch_sparse_decode(const ChessState& st, const Workspace& ws, int layer, c
   // cfg4/cfg5 and beyond 16 pages (the prefetches evict the running layer)
   static const int prefetch = getenv("CHESS_ATTN_PREFETCH") ? atoi(getenv("CHESS_ATTN_PREFETCH")) : 0;
   a.prefetch = prefetch;
+  a.next_pf = -1;  // set per mode in launch_inst
   const int gq = d.q_heads / d.kv_heads;
   static const int grid_env = getenv("CHESS_ATTN_GRID") ? atoi(getenv("CHESS_ATTN_GRID")) : 0;  // experiments
   const int nctas = grid_env > 0 ? std::min(grid_env, ws.attn_ctas) : ws.attn_ctas;
