@@ -501,6 +501,7 @@ def run_gpu(args):
             "unit": "GB/s",
             "frac": achieved / hbm_peak,
             "traffic": _ncu_traffic(cfg_name, "sparse_decode"),
+            "traffic_note": _ncu_traffic(cfg_name, "note"),
             "bytes_per_launch": attn_launch_bytes,
             "launch_us": attn_launch_s * 1e6,
             "tiles_per_launch": k4_tiles,
