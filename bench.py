@@ -486,6 +486,7 @@ def run_gpu(args):
             "kv_aliased": wl.aliased,
             "l2": "inputs larger than L2 (step reads >> 126 MB)",
             "ws_pages_mean": head["ws_mean"],
+            "ws_pages_min_max_at_kernel_timing": [int(wl_now.min()), int(wl_now.max())],
             "pre_roll_tokens": pre_roll,
             "generated_pages_sealed_before_timing": 4,
         },
