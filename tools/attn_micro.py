@@ -118,6 +118,12 @@ def main():
                 "sm_mhz": (lambda m: round(float(np.median((tb[m, 9] - tb[m, 8]) / (tb[m, 4] - tb[m, 2]) * 1e3)), 0) if m.any() else None)(ok_b & (tb[:, 8] > 0) & (tb[:, 4] > tb[:, 2])),
                 "cycles_spin_write_merge_push_arrive": [int(np.median(tb[ok_b & (tb[:, i] > 0), i])) if (ok_b & (tb[:, i] > 0)).any() else None for i in range(10, 15)],
                 "inbox": pct(tb[ok_b & (tb[:, 7] > 0), 7]) if (ok_b & (tb[:, 7] > 0)).any() else None}
+        if pattern == "random" and _lib.load().chess_debug_attn_trace(buf) == 0:
+            # per CTA of the last launch: SM id, streaming time (first page -> consumed)
+            tb = np.frombuffer(buf, dtype=np.uint64).reshape(2, 256, 16).astype(np.int64)[(L - 1) & 1]
+            ok = (tb[:, 3] > 0) & (tb[:, 2] > 0)
+            res["per_cta"] = [[int(c), int(tb[c, 15]), round((tb[c, 3] - tb[c, 2]) / 1e3, 2),
+                               round((tb[c, 4] - tb[ok, 0].min()) / 1e3, 2)] for c in np.nonzero(ok)[0]]
     res["bytes_per_launch"] = bytes_launch
     print(json.dumps(res))
 
