@@ -324,6 +324,9 @@ __global__ void __launch_bounds__(kThreads, CPS)
   if (kTrace && threadIdx.x == 0) {
 #pragma unroll
     for (int i = 1; i < 16; ++i) s_trace[i] = 0;
+    uint32_t smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    s_trace[15] = smid;  // which SM ran this CTA (per-CTA studies, tools/attn_micro.py)
     s_trace_warps = 0;
     if (blockIdx.x < 256)
       for (int i = 0; i < 16; ++i) g_attn_trace[args.layer & 1][blockIdx.x][i] = 0;
