@@ -733,6 +733,7 @@ __global__ void __launch_bounds__(kScanCTA, CHESS_SCAN_MINB) select_scan_kernel(
 // ---------------------------------------------------------------------------
 constexpr int kSmallRowBytes = 16384;  // rows up to this size use select_small_kernel
 constexpr int kSmallCand = 1024;       // select_small_kernel: candidates per level kept in shared memory
+constexpr int kSmallStageBytes = 128 * 1024;  // select_small_kernel: candidate rows staged per batch
 constexpr int kDescRing = 8;
 constexpr int kFlowMaxBatch = 256;  // per-slot scheduler tables live in shared memory
 constexpr int kDescEnd = -1, kDescFlush = -2;
@@ -1164,6 +1165,19 @@ __global__ void __launch_bounds__(kNT) select_small_kernel(ChessState st, Worksp
   __shared__ int s_cand[kSmallCand];
   __shared__ int s_plist[kSmallCand];
   __shared__ int s_cnt;
+  // a level's candidate rows are staged into shared memory (after the
+  // anchor) in batches of bulk copies: one memory latency per batch instead
+  // of one per row and warp (cfg1: every level is one batch)
+  __shared__ uint64_t s_rbar;
+  uint8_t* s_rows = reinterpret_cast<uint8_t*>(s_anc + ((d.dim + 15) & ~15));
+  const uint32_t row_bytes = (uint32_t)(((int64_t)d.dim * sizeof(T) + 15) & ~15);
+  const int batch_rows = (int)(kSmallStageBytes / row_bytes);
+  if (threadIdx.x == 0) {
+    mbar_init(&s_rbar, 1);
+    fence_barrier_init();
+  }
+  block_sync<kNT>();
+  uint32_t rphase = 0;
   int* stats = st.sel_stats + 8 * s;
   int m = sh.G;
   for (int lv = 0; lv < 3; ++lv) {
@@ -1173,15 +1187,26 @@ __global__ void __launch_bounds__(kNT) select_small_kernel(ChessState st, Worksp
     const void* b32 = lv == 0 ? (const void*)st.grid_vec32 : (lv == 1 ? (const void*)st.chunk_vec32 : (const void*)st.page_vec32);
     const int64_t lrows = lv == 0 ? max_grids(d) : (lv == 1 ? max_chunks(d) : (int64_t)d.max_pages);
     const T* base = reinterpret_cast<const T*>(sizeof(T) == 8 ? b64 : b32) + (int64_t)s * lrows * d.ld;
-    for (int i = warp; i < m; i += kNT / 32) {
-      const int id = lv == 0 ? i : s_cand[i];
-      const double acc = dot(base + (int64_t)id * d.ld);
-      if (lane == 0) {
-        sm.keys[i] = score_key(acc);
-        sc[i] = acc;
+    for (int b0 = 0; b0 < m; b0 += batch_rows) {
+      const int nr = min(batch_rows, m - b0);
+      if (threadIdx.x == 0) {
+        mbar_arrive_expect_tx(&s_rbar, (uint32_t)nr * row_bytes);
+        for (int r = 0; r < nr; ++r) {
+          const int id = lv == 0 ? b0 + r : s_cand[b0 + r];
+          tma_load_1d(s_rows + (size_t)r * row_bytes, base + (int64_t)id * d.ld, row_bytes, &s_rbar);
+        }
       }
+      mbar_wait(&s_rbar, rphase);
+      rphase ^= 1u;
+      for (int r = warp; r < nr; r += kNT / 32) {
+        const double acc = dot(reinterpret_cast<const T*>(s_rows + (size_t)r * row_bytes));
+        if (lane == 0) {
+          sm.keys[b0 + r] = score_key(acc);
+          sc[b0 + r] = acc;
+        }
+      }
+      block_sync<kNT>();  // the staging buffer is refilled by the next batch
     }
-    block_sync<kNT>();
     const int k = (int)ceil(prm.rho[lv] * (double)m);  // selection.py:98, 103, 108
     block_topk_mark<kNT>(sm.keys, m, k, sm.kept, sm.hist, sm.scratch);
     if (lv < 2) {
@@ -1657,14 +1682,17 @@ int launch_select(const ChessState& st, const Workspace& ws, const SelParams& pr
   static const int small_env = getenv("CHESS_SELECT_SMALL") ? atoi(getenv("CHESS_SELECT_SMALL")) : 1;
   if (small_env && !prm.full_scan && !prm.xout && !prm.xpeer && prm.mode == 0 &&
       st.d.ld * summary_elem_bytes(st.d.summary_dtype) <= kSmallRowBytes) {
-    // dynamic shared memory: the slot's anchor (d.dim doubles, <= 32 KB)
-    const size_t dyn = (size_t)st.d.dim * sizeof(double);
+    // dynamic shared memory: the slot's anchor (d.dim doubles, <= 64 KB) and
+    // the row staging buffer
+    const size_t dyn = (size_t)((st.d.dim + 15) & ~15) * sizeof(double) + kSmallStageBytes;
     static bool configured = false;
     if (!configured) {
-      cudaFuncSetAttribute(select_small_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmallRowBytes * 2);
+      cudaFuncSetAttribute(select_small_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           kSmallRowBytes * 2 + kSmallStageBytes);
       cudaFuncSetAttribute(select_small_kernel<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           kSmallRowBytes * 4);
-      cudaFuncSetAttribute(select_small_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmallRowBytes);
+                           kSmallRowBytes * 4 + kSmallStageBytes);
+      cudaFuncSetAttribute(select_small_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           kSmallRowBytes + kSmallStageBytes);
       configured = true;
     }
     if (st.d.summary_dtype == 0)
