@@ -691,11 +691,13 @@ def run_plumbing(args):
 
 
 # --summary-dtype auto: the measured-faster selection path per config
-# (profiles/r02/dtype_sweep/summary.txt, one box): the tensor-core scan halves
-# the selection's bytes but runs 7 launches with 6 per-slot tails instead of 3;
-# only at cfg3 (16 x 4096 pages of 32768-wide rows) do the bytes win
-# (787 vs 873 us/step); at cfg1/cfg2/cfg4/cfg5 f32 mirrors are faster.
-AUTO_DTYPE = {"cfg3": "f16tc"}
+# (profiles/r02/dtype_sweep/summary.txt, one box, with the tensor-core scan on
+# 96 CTAs next to the decode): the tensor-core scan halves the selection's
+# bytes but runs 7 launches with 6 per-slot tails instead of 3, so it wins
+# where the bytes dominate — cfg3 776 vs 873 us/step, cfg4 2082 vs 2140,
+# cfg5 1202 vs 1299 — and loses at batch 1 / short rows (cfg2 170 vs 136,
+# cfg1 43.6 vs 40.3), where f32 mirrors stay.
+AUTO_DTYPE = {"cfg3": "f16tc", "cfg4": "f16tc", "cfg5": "f16tc"}
 
 DTYPES = {
     "f16tc": "bf16 KV / fp16 summary mirrors on tcgen05 (certified bounds) + exact f64 rescoring near each cut",
@@ -718,7 +720,7 @@ def main():
                     help="f16tc: fp16 mirrors scored on tcgen05 with certified bounds, exact f64 rescoring "
                          "near each cut (selections identical to the f64 scores); f32: f32 mirrors on CUDA "
                          "cores.  auto (default): the faster of the two per config, measured "
-                         "(profiles/r02/dtype_sweep/summary.txt): f16tc at cfg3, f32 elsewhere")
+                         "(profiles/r02/dtype_sweep/summary.txt): f16tc at cfg3/cfg4/cfg5, f32 at cfg1/cfg2")
     ap.add_argument("--full-scan", action="store_true")
     ap.add_argument("--headline-only", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
