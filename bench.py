@@ -734,6 +734,10 @@ def main():
     args = ap.parse_args()
     if args.summary_dtype == "auto":
         args.summary_dtype = AUTO_DTYPE.get(args.config, "f32")
+        # the KV-head shard exchanges partial f64 scores per level (f32 / f64
+        # scan paths); the tensor-core scan is single-rank
+        if _shard_plan(args, _dist_env()[1])[0] == "head":
+            args.summary_dtype = "f32"
     if args.warmup < 3:
         args.warmup = 3
     env_world = os.environ.get("WORLD_SIZE")
