@@ -92,7 +92,6 @@ struct AttnArgs {
   int layer;
   int cl;    // cluster-merge mode: CTAs per segment (= cluster size), 0 = off
   int prefetch;  // pages past the first run prefetched into L2 before the PDL wait
-  int next_pf;   // pages of the CTA's range prefetched into L2 for layer + 1 once its own loads are issued
   // Head-shard output gather over peer memory (chess_sparse_decode_gather):
   // every output row is also stored at the same offset from peer_out[p]
   // (this rank's block in peer p's region, NVLink stores).
@@ -103,6 +102,10 @@ struct AttnArgs {
               // K/V loads may run before griddepcontrol.wait; 0: wait first (e.g. after an
               // append, which writes the tail row, tail_fill and the block table)
   int mode;  // debug (CHESS_ATTN_MODE): 0 normal, 1 loads only (no math), 2 math only (no K/V loads), 5 exit at entry, 6 exit after the prologue, 7 force stream-K, 8 no PDL wait (timing only: ignores the previous kernel)
+  int next_pf;  // pages of the CTA's range prefetched into L2 for layer + 1 once its own loads are issued
+  // (New fields go here, at the end: inserting next_pf before peer_out moved
+  // the parameter offsets and changed the cluster instance's code generation,
+  // 178 -> 167 registers, cfg2 K4 3.1 -> 3.4 us; A/B in profiles/r02/k4_next_layer_prefetch.txt.)
 };
 
 // one bf16 pair of an output row, to this rank's buffer and (PEERS: the
@@ -562,12 +565,14 @@ __global__ void __launch_bounds__(kThreads, CPS)
     // same position: once this layer's loads are all issued (the ring only
     // drains from here), pull the next layer's first tiles into L2 so that
     // layer's start hits L2 instead of HBM (an L2 hint: no data dependency).
-    if (args.next_pf > 0 && args.layer + 1 < d.layers && n > 0) {
-      int row0, tag;
-      fetch(0, row0, tag);
-      if (lane < min(args.next_pf, min(n, 32))) {
-        tma_prefetch_4d(&kmap, 0, row0, 0, args.layer + 1);
-        tma_prefetch_4d(&vmap, 0, row0, 0, args.layer + 1);
+    if constexpr (!XC) {  // piece mode only (the work split of the cluster instance differs)
+      if (args.next_pf > 0 && args.layer + 1 < d.layers && n > 0) {
+        int row0, tag;
+        fetch(0, row0, tag);
+        if (lane < min(args.next_pf, min(n, 32))) {
+          tma_prefetch_4d(&kmap, 0, row0, 0, args.layer + 1);
+          tma_prefetch_4d(&vmap, 0, row0, 0, args.layer + 1);
+        }
       }
     }
     return;
