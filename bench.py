@@ -492,7 +492,9 @@ def run_gpu(args):
         },
         "bytes_per_step": bytes_step,
         "step_roofline": {"achieved": bytes_step / (ms_step / 1e3) / 1e9, "peak": hbm_peak, "unit": "GB/s",
-                          "frac": bytes_step / (ms_step / 1e3) / 1e9 / hbm_peak},
+                          "frac": bytes_step / (ms_step / 1e3) / 1e9 / hbm_peak,
+                          # the north star's "about 8 TB/s" nominal, for context
+                          "frac_of_nominal_8tbs": bytes_step / (ms_step / 1e3) / 1e9 / 8000.0},
         "roofline": {
             "kernel": "sparse_decode (K4)",
             "bound": "hbm",
@@ -501,6 +503,7 @@ def run_gpu(args):
             "peak_source": peak_src,
             "unit": "GB/s",
             "frac": achieved / hbm_peak,
+            "frac_of_nominal_8tbs": achieved / 8000.0,
             "traffic": _ncu_traffic(cfg_name, "sparse_decode"),
             "traffic_note": _ncu_traffic(cfg_name, "note"),
             "bytes_per_launch": attn_launch_bytes,
