@@ -284,5 +284,18 @@ def test_tc_select_at_bench_cfg3_state():
         pages, _ = ref.working_set(sel, P, cfg.window_pages, 1)
         np.testing.assert_array_equal(st.ws_logical[s, : int(st.ws_len[s])].cpu().numpy(), pages)
         np.testing.assert_array_equal(st.block_table[s, : len(pages)].cpu().numpy(), wl.table_cpu[s, pages].numpy())
+    # the engine's overlapped step runs the same pass with deferred working
+    # sets on fewer CTAs (96 of 148): identical selections, working sets after
+    # the flush
+    want = st.semantic.clone(), st.n_semantic.clone(), st.ws_logical.clone(), st.block_table.clone()
+    st.semantic.fill_(-1)
+    dec.select(force_all=True, defer_ws=True)
+    _lib.call("chess_flush_working_sets", st.ref, _lib.stream_ptr())
+    torch.cuda.synchronize()
+    assert torch.equal(st.n_semantic, want[1])
+    for s in range(16):
+        n = int(want[1][s])
+        assert torch.equal(st.semantic[s, :n], want[0][s, :n]), s
+    assert torch.equal(st.ws_logical, want[2]) and torch.equal(st.block_table, want[3])
     del wl, st, dec
     torch.cuda.empty_cache()
