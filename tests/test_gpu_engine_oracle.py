@@ -33,6 +33,7 @@ import torch
 
 from oracle import attention as attn_ref
 from oracle import pagesel_ref as ref
+from paper_2602_20732_b200 import _lib
 from paper_2602_20732_b200.config import preset_config
 from paper_2602_20732_b200.engine import ChessDecoder
 from paper_2602_20732_b200.state import DecodeState, Shape
@@ -43,6 +44,7 @@ L, H, HQ, HD, B = 2, 8, 8, 64, 16  # cfg1 (BASELINE configs[0]) model shape
 D = L * H * HD
 P_CTX, G_PAGES, BATCH = 96, 10, 2
 SCHEDULES = [((2, 2.0), (5, 2.0), (8, 3.0)), ((4, 2.0),)]
+_LAST_STATE = [None]  # the state of the last decode-loop test (for path checks)
 NAMES = {1: "semantic", 2: "window", 3: "sink"}
 
 
@@ -145,6 +147,7 @@ def test_engine_decode_matches_oracle_loop(policy, mode, summary_dtype):
     max_pages = P_CTX + G_PAGES + 2
     table = rng.permutation(BATCH * max_pages).reshape(BATCH, max_pages)
     st = _make_state(loads, summary_dtype, table)
+    _LAST_STATE[0] = st
 
     th = SimpleNamespace(tau_entropy=tau[0], tau_varentropy=tau[1]) if tau else None
     dec = ChessDecoder(st, cfg, policy=policy, thresholds=th,
@@ -244,3 +247,30 @@ def test_engine_decode_matches_oracle_loop(policy, mode, summary_dtype):
 
 def _rows_to_flat(rows_bf16):
     return rows_bf16.reshape(rows_bf16.shape[0], D)
+
+
+@pytest.mark.parametrize("policy", ["always", "dynamic"])
+def test_engine_decode_tensor_core_scan_matches_oracle(policy):
+    """The same product-path check at a key width whose summary rows go
+    through the tensor-core scan (4 layers x 8 kv heads x head_dim 128: D =
+    4096, f64 rows of 32 KB > the 16 KB short-row path): the overlapped
+    engine step with fp16 tcgen05 scoring and exact f64 rescoring selects,
+    triggers and builds working sets exactly as the f64 oracle decode loop."""
+    global L, H, HQ, HD, D
+    saved = (L, H, HQ, HD, D)
+    L, H, HQ, HD = 4, 8, 8, 128
+    D = L * H * HD
+    try:
+        test_engine_decode_matches_oracle_loop(policy, "concurrent", "f16tc")
+        # the tensor-core tail ran: it records each slot's page-level candidate count
+        import ctypes as C
+        lib = _lib.load()
+        lib.chess_debug_tc_read.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.c_int32] + [C.c_void_p] * 5
+        meta = np.zeros(4, np.int32)
+        st = _LAST_STATE[0]
+        for s in range(BATCH):
+            _lib.check(lib.chess_debug_tc_read(st.ref, s, 0, 0, None, None, None, meta.ctypes.data, None), "tc_read")
+            assert meta[2] > 0, (s, meta)
+    finally:
+        L, H, HQ, HD, D = saved
+        _LAST_STATE[0] = None
