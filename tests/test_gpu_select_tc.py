@@ -256,6 +256,32 @@ def test_tc_accumulation_error_model():
     assert ratio.max() <= GAMMA_MODEL
 
 
+def test_tc_select_at_bench_cfg5_state():
+    """cfg5's state (Llama-3-70B shape: D = 80 x 8 x 128 = 81920, 40 slices
+    of 2048; P = 4096; batch 8), where the bench also runs the tensor-core
+    selection: every slot's selection equals the f64 cascade."""
+    from paper_2602_20732_b200.engine import ChessDecoder
+    from paper_2602_20732_b200.synthetic import SyntheticDecode
+
+    wl = SyntheticDecode("cfg5", batch=8, gen_pages=4, ring=2, kv_budget_gib=8, summary_dtype="f16tc")
+    st, sh = wl.st, wl.shape
+    cfg = preset_config("aggressive", page_size=sh.page_size)
+    dec = ChessDecoder(st, cfg, policy="every_step")
+    wl.prefill(dec)
+    P, D = wl.P, sh.dim
+    Cn = math.ceil(P / 8)
+    G = math.ceil(Cn / 8)
+    p2c, c2g = np.arange(P) // 8, np.arange(Cn) // 8
+    for s in range(8):
+        sc = [torch.mv(m[s, :n, :D], st.anchor[s, :D]).cpu().numpy()
+              for m, n in ((st.grid_vec64, G), (st.chunk_vec64, Cn), (st.page_vec64, P))]
+        sel, _ = ref.prune(sc[0], sc[1], sc[2], p2c, c2g, cfg.ratios)
+        sem = st.semantic[s, : int(st.n_semantic[s])].cpu().numpy()
+        np.testing.assert_array_equal(sem, sel, err_msg=f"slot {s}")
+    del wl, st, dec
+    torch.cuda.empty_cache()
+
+
 def test_tc_select_at_bench_cfg3_state():
     """The bench's headline state (cfg3: D = 32768, P = 4096, batch 16,
     planted relevance, built by K1b) with fp16 tensor-core scoring: every
