@@ -1634,7 +1634,12 @@ static int launch_select_tc(const ChessState& st, const Workspace& ws, const Sel
   // 779-782 at 80-88 / 104-112 and 797 at 64-72; the pass alone is faster
   // on every SM (328 vs 373 us), which is what a standalone selection gets.
   static const int grid_override = getenv("CHESS_SELECT_GRID") ? atoi(getenv("CHESS_SELECT_GRID")) : 0;  // A/B
-  const int grid = grid_override > 0 ? grid_override : (prm.defer_ws ? std::max(1, num_sms() * 96 / 148) : num_sms());
+  // With more segments than SMs the decode runs two CTAs per SM (stream-K)
+  // and the scan does best on 72 (cfg4: 2034 us at 72, 2058 at 64, 2083 at 96,
+  // 2097 at 148, 2148 at 48).
+  const int segs = d.batch * d.kv_heads;
+  const int share = segs > num_sms() ? 72 : 96;
+  const int grid = grid_override > 0 ? grid_override : (prm.defer_ws ? std::max(1, num_sms() * share / 148) : num_sms());
   for (int level = 0; level < 3; ++level) {
     select_tc_kernel<<<grid, kTcCTA, tc_smem(d.batch), stream>>>(st, ws, prm, level, mg, mc, mp);
     if ((rc = check_launch("select_tc"))) return rc;
