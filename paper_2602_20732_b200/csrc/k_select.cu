@@ -1546,7 +1546,13 @@ static int launch_scan(const ChessState& st, const Workspace& ws, const SelParam
     configured = true;
   }
   static const int grid_override = getenv("CHESS_SELECT_GRID") ? atoi(getenv("CHESS_SELECT_GRID")) : 0;  // debug
-  const int grid = grid_override > 0 ? grid_override : (grid_default > 0 ? grid_default : num_sms());
+  // Next to a concurrent decode at small batch (its cluster grid is a
+  // quarter of the SMs or less: cfg2) the scan does best on 64 CTAs: cfg2
+  // step 115-117 us at 24..64 against 122 at 148 (profiles/r02/select_grid_sweep.txt).
+  const bool small_batch_overlap = prm.defer_ws && st.d.batch * st.d.kv_heads * 4 <= num_sms();
+  const int grid = grid_override > 0 ? grid_override
+                   : grid_default > 0 ? grid_default
+                   : small_batch_overlap ? std::max(1, num_sms() * 64 / 148) : num_sms();
   select_scan_kernel<T><<<grid, kScanCTA, smem, stream>>>(st, ws, prm, level);
   return check_launch("select_scan");
 }
