@@ -558,6 +558,15 @@ def run_gpu(args):
                    "triggers_fired": r["triggers"]}
             for name, r in results.items()
         }
+        # what selecting every step costs inside the overlapped step: the
+        # time over the attention-only step, against the selection's bytes
+        extra_us = ms_step * 1e3 - out["variants"]["attn_only"]["us_per_step"]
+        if extra_us > 0:
+            out["select_marginal"] = {
+                "us_per_step": extra_us, "bytes": sel_call_bytes,
+                "achieved": sel_call_bytes / (extra_us / 1e6) / 1e9, "unit": "GB/s",
+                "frac": sel_call_bytes / (extra_us / 1e6) / 1e9 / hbm_peak,
+            }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(cfg_name, steps=1)
     if rank == 0:
