@@ -216,10 +216,12 @@ __global__ void __launch_bounds__(kNT) entropy_kernel(ChessState st, Workspace w
   }
 }
 
-// CTAs per row: enough to fill the GPU twice for small batches, and slices of
-// at most 4 register chunks per thread
+// CTAs per row: one CTA per SM over all rows for small batches, and slices
+// of at most 4 register chunks per thread.  (Two per SM, the round-1 choice,
+// measured the same: cfg3 8.7 vs 8.5 us in the step timeline, step 769.3 vs
+// 770.6 us; one per SM leaves more room to the kernels running beside it.)
 int ent_splits(int64_t rows, int64_t vocab) {
-  const int64_t by_gpu = (2 * (int64_t)num_sms() + rows - 1) / std::max<int64_t>(rows, 1);
+  const int64_t by_gpu = (int64_t)num_sms() / std::max<int64_t>(rows, 1);
   const int64_t by_vocab = (vocab + 4 * 4 * kEntVec * kNT - 1) / (4 * 4 * kEntVec * kNT);
   return (int)std::min<int64_t>(kEntSplit, std::max<int64_t>({(int64_t)4, by_gpu, by_vocab}));
 }

@@ -193,10 +193,30 @@ __global__ void __launch_bounds__(kNT) append_kernel(ChessState st, const __nv_b
                                                      int post) {
   __shared__ int s_scratch[48];
   __shared__ int s_last;
+  // The decode layer that follows (K4, launched with programmatic stream
+  // serialization) may launch now: it executes griddepcontrol.wait before it
+  // reads any state this kernel writes, so only its launch latency overlaps.
+  pdl_launch_dependents();
   const int s = blockIdx.y;
   if (active && !active[s]) return;
   const ChessDims& d = st.d;
   const int B = d.page_size;
+  // The token's columns and their running key sums do not depend on the
+  // counters: load them first, so that the counter reads, these loads and
+  // the key-sum reads share one memory round trip (the stores below would
+  // otherwise keep the key-sum loads behind them).
+  const int64_t cend_ = col0 + ncols;
+  const int64_t j0_ = col0 + ((int64_t)blockIdx.x * kNT + threadIdx.x) * 8;
+  const bool vec = (d.head_dim % 8) == 0 && (row_stride % 8) == 0 && (d.ld % 2) == 0;
+  uint4 kv_pre = make_uint4(0, 0, 0, 0), vv_pre = kv_pre;
+  double2 ks_pre[4];
+  if (vec && j0_ < cend_) {
+    kv_pre = __ldcs(reinterpret_cast<const uint4*>(k_rows + (int64_t)s * row_stride - col0 + j0_));
+    vv_pre = __ldcs(reinterpret_cast<const uint4*>(v_rows + (int64_t)s * row_stride - col0 + j0_));
+    const double2* k2 = reinterpret_cast<const double2*>(st.key_sum + (int64_t)s * d.ld + j0_);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) ks_pre[q] = k2[q];
+  }
   const int np = st.num_pages[s];
   const int fill = st.tail_fill[s];
   bool open_new;
@@ -226,19 +246,19 @@ __global__ void __launch_bounds__(kNT) append_kernel(ChessState st, const __nv_b
 
   const int64_t j0 = col0 + ((int64_t)blockIdx.x * kNT + threadIdx.x) * 8;
   if (j0 < cend) {
-    if ((d.head_dim % 8) == 0 && (row_stride % 8) == 0) {
-      const uint4 kv = *reinterpret_cast<const uint4*>(kr + j0);
-      const uint4 vv = *reinterpret_cast<const uint4*>(vr + j0);
+    if (vec) {
       const int64_t off = pool_offset(d, j0, phys, row);
-      *reinterpret_cast<uint4*>(kp + off) = kv;
-      *reinterpret_cast<uint4*>(vp + off) = vv;
-      const uint32_t w[4] = {kv.x, kv.y, kv.z, kv.w};
+      *reinterpret_cast<uint4*>(kp + off) = kv_pre;
+      *reinterpret_cast<uint4*>(vp + off) = vv_pre;
+      const uint32_t w[4] = {kv_pre.x, kv_pre.y, kv_pre.z, kv_pre.w};
+      double2* k2 = reinterpret_cast<double2*>(ks + j0);
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         const float2 f = bf2x2f(w[q]);
-        const int64_t j = j0 + 2 * q;
-        ks[j] = open_new ? (double)f.x : __dadd_rn(ks[j], (double)f.x);
-        ks[j + 1] = open_new ? (double)f.y : __dadd_rn(ks[j + 1], (double)f.y);
+        double2 o;
+        o.x = open_new ? (double)f.x : __dadd_rn(ks_pre[q].x, (double)f.x);
+        o.y = open_new ? (double)f.y : __dadd_rn(ks_pre[q].y, (double)f.y);
+        k2[q] = o;
       }
     } else {
       for (int q = 0; q < 8; ++q) {

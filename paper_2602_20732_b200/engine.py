@@ -291,13 +291,15 @@ class ChessDecoder:
 
     # ------------------------------------------------------------------
     def capture(self, k_new, v_new, q, logits, out, lse=None, entropy_out=None, entropies=None):
-        """Capture `step` on static buffers as one CUDA graph."""
-        g = torch.cuda.CUDAGraph()
+        """Capture `step` on static buffers as one CUDA graph (the graph
+        definition is kept, so its nodes and edges can be inspected)."""
+        g = torch.cuda.CUDAGraph(keep_graph=True)
         s = torch.cuda.Stream()
         s.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(s):
             with torch.cuda.graph(g, stream=s):
                 self.step(k_new, v_new, q, logits, out, lse, entropy_out, stream=s, entropies=entropies)
         torch.cuda.current_stream().wait_stream(s)
+        g.instantiate()
         self.graph = g
         return g
