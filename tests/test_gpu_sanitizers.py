@@ -20,6 +20,11 @@ REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 def _sanitizer():
+    # opt-in: the GPU pool closed compute-sanitizer after runs under it left
+    # GPUs needing a reset, so the default GPU suite never launches it (the
+    # committed logs under profiles/r02/sanitizers/ are the evidence)
+    if os.environ.get("CHESS_RUN_SANITIZERS") != "1":
+        pytest.skip("compute-sanitizer runs are opt-in (CHESS_RUN_SANITIZERS=1)")
     exe = shutil.which("compute-sanitizer") or "/usr/local/cuda/bin/compute-sanitizer"
     if not os.path.exists(exe):
         pytest.skip("compute-sanitizer not found")
@@ -34,6 +39,8 @@ def test_smoke_under_sanitizer(tool):
                        [exe, "--tool", tool, sys.executable, "-c", "import __graft_entry__ as g; g.smoke()"],
                        cwd=REPO, capture_output=True, text=True, timeout=900)
     out = r.stdout + r.stderr
+    if "closed on this pool" in out:
+        pytest.skip("compute-sanitizer is closed on this GPU pool")
     assert r.returncode == 0, out[-3000:]
     assert "smoke ok" in out, out[-3000:]
     summary = [l for l in out.splitlines() if "SUMMARY" in l]
