@@ -57,16 +57,26 @@ def build(verbose: bool = False, force: bool = False, trace: bool = False, varia
         lib = PKG_DIR / f"libchess_b200_{variant}.so"
         extra += [f"-D{x}" for x in defines]
     bdir.mkdir(parents=True, exist_ok=True)
-    objs = []
+    objs, todo = [], []
     for src in SOURCES:
         s = CSRC / src
         o = bdir / (s.stem + ".o")
         objs.append(o)
         if force or _stale(o, [s, *HEADERS]):
-            cmd = [NVCC, *ARCH, *FLAGS, *extra, "-c", str(s), "-o", str(o)]
-            res = subprocess.run(cmd, capture_output=True, text=True)
-            log = bdir / (s.stem + ".ptxas.log")
-            log.write_text(res.stdout + res.stderr)
+            todo.append((src, s, o))
+
+    def compile_one(job):
+        src, s, o = job
+        cmd = [NVCC, *ARCH, *FLAGS, *extra, "-c", str(s), "-o", str(o)]
+        res = subprocess.run(cmd, capture_output=True, text=True)
+        (bdir / (s.stem + ".ptxas.log")).write_text(res.stdout + res.stderr)
+        return src, res
+
+    # the translation units are independent: compile them concurrently
+    from concurrent.futures import ThreadPoolExecutor
+
+    with ThreadPoolExecutor(max_workers=max(1, min(len(todo), os.cpu_count() or 1))) as ex:
+        for src, res in ex.map(compile_one, todo):
             if res.returncode != 0:
                 sys.stderr.write(res.stdout + res.stderr)
                 raise RuntimeError(f"nvcc failed on {src}")

@@ -165,6 +165,21 @@ __device__ __forceinline__ uint64_t score_key(double s) {
   uint64_t b = (uint64_t)__double_as_longlong(s);
   return (b & 0x8000000000000000ull) ? ~b : (b | 0x8000000000000000ull);
 }
+// inverse of score_key on non-NaN values
+__device__ __forceinline__ double double_of_key(uint64_t k) {
+  const uint64_t b = (k & 0x8000000000000000ull) ? (k ^ 0x8000000000000000ull) : ~k;
+  return __longlong_as_double((long long)b);
+}
+// order-preserving 32-bit key of a float (-0 and +0 equal, NaN lowest) and its inverse
+__device__ __forceinline__ uint32_t float_key(float f) {
+  if (f != f) return 0u;
+  if (f == 0.0f) f = 0.0f;
+  const uint32_t b = __float_as_uint(f);
+  return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
+__device__ __forceinline__ float float_of_key(uint32_t k) {
+  return __uint_as_float((k & 0x80000000u) ? (k ^ 0x80000000u) : ~k);
+}
 
 // NumPy pairwise summation of a contiguous f64 vector (numpy
 // DOUBLE_pairwise_sum, blocks of 8 accumulators up to 128 elements).  Used for
@@ -442,6 +457,32 @@ __device__ __forceinline__ int block_exclusive_scan(int v, int* smem_warp, int* 
   *total = smem_warp[NT / 32 - 1];
   block_sync<NT>();
   return base + x - v;
+}
+
+// Block-wide bitonic sort of two arrays of n2 (a power of two, >= 2) 32-bit
+// keys in shared memory, both descending, side by side: log2(n2)(log2(n2)+1)/2
+// compare-exchange stages, one barrier each for both arrays.
+template <int NT>
+__device__ void block_sort2_desc_u32(uint32_t* a, uint32_t* b, int n2) {
+  for (int size = 2; size <= n2; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int t = threadIdx.x; t < (n2 >> 1); t += NT) {
+        const int i = 2 * t - (t & (stride - 1));
+        const int j = i + stride;
+        const bool desc = (i & size) == 0;
+        const uint32_t x = a[i], y = a[j], u = b[i], v = b[j];
+        if (desc ? (x < y) : (x > y)) {
+          a[i] = y;
+          a[j] = x;
+        }
+        if (desc ? (u < v) : (u > v)) {
+          b[i] = v;
+          b[j] = u;
+        }
+      }
+      block_sync<NT>();
+    }
+  }
 }
 
 constexpr int kRankTopkMax = 64;  // rank-count top-k up to this many candidates

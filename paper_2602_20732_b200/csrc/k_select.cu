@@ -1831,6 +1831,12 @@ extern "C" int chess_debug_select_trace(unsigned long long* host_out) {
   return cudaMemcpyFromSymbol(host_out, chess::g_sel_trace, sizeof(chess::g_sel_trace)) == cudaSuccess ? 0 : 8;
 }
 
+// trace build: [3][256][4] per-CTA stamps of the tensor-core scan, then [3][64][12] per-slot tails
+extern "C" int chess_debug_select_tc_trace(unsigned long long* host_out) {
+  if (cudaMemcpyFromSymbol(host_out, chess::g_tc_trace, sizeof(chess::g_tc_trace)) != cudaSuccess) return 8;
+  return cudaMemcpyFromSymbol(host_out + 3 * 256 * 4, chess::g_tc_tail, sizeof(chess::g_tc_tail)) == cudaSuccess ? 0 : 8;
+}
+
 extern "C" int chess_debug_select_tail_trace(unsigned long long* host_out) {
   return cudaMemcpyFromSymbol(host_out, chess::g_tail_trace, sizeof(chess::g_tail_trace)) == cudaSuccess ? 0 : 8;
 }

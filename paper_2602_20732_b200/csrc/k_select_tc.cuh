@@ -60,6 +60,17 @@ struct TcTile {
   int s, n, g0, ng, slice;
 };
 
+// Debug timeline (trace build only, chess_debug_select_tc_trace): per CTA of
+// the last tensor-core launch of each level {entry, items done, exit, tails
+// run}, and per slot {tail start, tail end, CTA, items left in that CTA's
+// range when it won the slot}.
+__device__ unsigned long long g_tc_trace[3][256][4];
+__device__ unsigned long long g_tc_tail[3][64][12];
+// tail phase stamps [4..9]: norms, rows certified, T, H, classified, emitted
+__device__ __forceinline__ void tc_tail_stamp(int lv, int s, int which) {
+  if (kTrace && threadIdx.x == 0 && s < 64) g_tc_tail[lv][s][which] = global_ns();
+}
+
 // tiles of one slot's level: groups of 8 candidates, spread evenly over
 // ceil(groups / 16) tiles
 __device__ __forceinline__ int tc_tiles(int n) {
@@ -225,19 +236,35 @@ __device__ void tc_tail(const ChessState& st, const Workspace& ws, const SelPara
   int* kept = in_smem ? sm.kept : ws.kept + (int64_t)s * mr;
   int* cls = ws.cls + (int64_t)s * mr;
   int* meta = ws.unc_meta + 4 * s;
+  // slice sums of the anchor statistics in slice order: the slices' loads in
+  // parallel (one round trip, staged in sm.keys before it holds keys), the
+  // sums by thread 0
+  double* s_st = reinterpret_cast<double*>(sm.keys);
+  const bool par_norm = 3 * nsl <= kTailCap;
+  if (par_norm) {
+    for (int q = threadIdx.x; q < nsl; q += kNT) {
+      const double* t = ws.anc_stats + ((int64_t)s * nsl + q) * 4;
+      s_st[3 * q] = __ldcg(t);
+      s_st[3 * q + 1] = __ldcg(t + 1);
+      s_st[3 * q + 2] = __ldcg(t + 2);
+    }
+    block_sync<kNT>();
+  }
   if (threadIdx.x == 0) {
     double a2 = 0.0, r2 = 0.0, p2 = 0.0;
     for (int q = 0; q < nsl; ++q) {
-      const double* t = ws.anc_stats + ((int64_t)s * nsl + q) * 4;
-      a2 += t[0];
-      r2 += t[1];
-      p2 += t[2];
+      const double* t = par_norm ? s_st + 3 * q : nullptr;
+      const double* g = ws.anc_stats + ((int64_t)s * nsl + q) * 4;
+      a2 += par_norm ? t[0] : __ldcg(g);
+      r2 += par_norm ? t[1] : __ldcg(g + 1);
+      p2 += par_norm ? t[2] : __ldcg(g + 2);
     }
     s_norm[0] = sqrt(a2) * (1.0 + 0x1p-20);
     s_norm[1] = sqrt(r2) * (1.0 + 0x1p-20);
     s_norm[2] = sqrt(p2) * (1.0 + 0x1p-20);
   }
   block_sync<kNT>();
+  tc_tail_stamp(lv, s, 4);
   const double A = s_norm[0], Rem = s_norm[1], Sp = s_norm[2];
   const int k = (int)ceil(prm.rho[lv] * (double)n);  // selection.py:98, 103, 108
   if (k >= n) {
@@ -247,56 +274,118 @@ __device__ void tc_tail(const ChessState& st, const Workspace& ws, const SelPara
     tc_emit_level(st, ws, prm, s, lv, n, kept, sm);
     return;
   }
-  // intervals [lo, hi] around the certified approximate score; hi kept in
-  // the first slice partial of the row (consumed)
-  for (int i = threadIdx.x; i < n; i += kNT) {
-    double* pr = part + (int64_t)i * nsl;
-    double acc = 0.0;
-    for (int q = 0; q < nsl; ++q) acc = q ? __dadd_rn(acc, __ldcg(pr + q)) : __ldcg(pr);
-    const int id = cand ? cand[i] : i;
-    const double* stash = tc_row_stash(st, s, lv, id);
-    const double err = stash[0], nrm = stash[1];
-    const double e = A * err + (Rem + kGammaTc * Sp) * nrm + 0x1p-38 * (A * (nrm + err) + Sp * nrm);
-    double lo = acc - e, hi = acc + e;
-    if (!(isfinite(acc) && isfinite(e))) {
-      lo = -INFINITY;
-      hi = INFINITY;
+  // intervals [lo, hi] around the certified approximate score (lo in
+  // ws.scores, over the row's err stash; hi in the row's first slice
+  // partial, consumed).  Two rows per thread iteration with every load issued
+  // before use: the 16 slice partials of each row and the {err, nrm} the
+  // scan's slice-0 epilogue gathered (ws.scores / ws.keys at the position).
+  // Up to kTailCap candidates the bound keys also go to shared memory as
+  // conservative 32-bit keys (lo rounded down, hi rounded up, below).
+  uint32_t* k32 = reinterpret_cast<uint32_t*>(sm.keys);  // [0, 1024) lo, [1024, 2048) hi
+  const double* nrm_v = reinterpret_cast<const double*>(ws.keys) + (int64_t)s * mr;
+  for (int i0 = threadIdx.x; i0 < n; i0 += 2 * kNT) {
+    const int i1 = i0 + kNT;
+    const bool has1 = i1 < n;
+    const int j1 = has1 ? i1 : i0;
+    double* pr0 = part + (int64_t)i0 * nsl;
+    double* pr1 = part + (int64_t)j1 * nsl;
+    const double err0 = __ldcg(lo_v + i0), nrm0 = __ldcg(nrm_v + i0);
+    const double err1 = __ldcg(lo_v + j1), nrm1 = __ldcg(nrm_v + j1);
+    double acc0 = 0.0, acc1 = 0.0;
+    for (int q0 = 0; q0 < nsl; q0 += 16) {
+      double v0[16], v1[16];
+#pragma unroll
+      for (int q = 0; q < 16; ++q) {
+        v0[q] = q0 + q < nsl ? __ldcg(pr0 + q0 + q) : 0.0;
+        v1[q] = q0 + q < nsl ? __ldcg(pr1 + q0 + q) : 0.0;
+      }
+      acc0 = q0 ? __dadd_rn(acc0, v0[0]) : v0[0];
+      acc1 = q0 ? __dadd_rn(acc1, v1[0]) : v1[0];
+#pragma unroll
+      for (int q = 1; q < 16; ++q)
+        if (q0 + q < nsl) {
+          acc0 = __dadd_rn(acc0, v0[q]);
+          acc1 = __dadd_rn(acc1, v1[q]);
+        }
     }
-    lo_v[i] = lo;
-    pr[0] = hi;
-    keys[i] = score_key(lo);
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      if (r == 1 && !has1) break;
+      const double acc = r ? acc1 : acc0, err = r ? err1 : err0, nrm = r ? nrm1 : nrm0;
+      const int i = r ? i1 : i0;
+      const double e = A * err + (Rem + kGammaTc * Sp) * nrm + 0x1p-38 * (A * (nrm + err) + Sp * nrm);
+      double lo = acc - e, hi = acc + e;
+      if (!(isfinite(acc) && isfinite(e))) {
+        lo = -INFINITY;
+        hi = INFINITY;
+      }
+      lo_v[i] = lo;
+      (r ? pr1 : pr0)[0] = hi;
+      if (in_smem) {
+        k32[i] = float_key(__double2float_rd(lo));
+        k32[kTailCap + i] = float_key(__double2float_ru(hi));
+      } else {
+        keys[i] = score_key(lo);
+      }
+    }
   }
   block_sync<kNT>();
-  // T = k-th largest lower bound
-  block_topk_mark<kNT>(keys, n, k, kept, sm.hist, sm.scratch);
-  uint64_t tk = ~0ull;
-  for (int i = threadIdx.x; i < n; i += kNT)
-    if (kept[i]) tk = min(tk, keys[i]);
-  for (int o = 16; o > 0; o >>= 1) tk = min(tk, (uint64_t)__shfl_xor_sync(0xffffffffu, (unsigned long long)tk, o));
-  __shared__ unsigned long long s_tk[kWarps];
-  if ((threadIdx.x & 31) == 0) s_tk[threadIdx.x >> 5] = tk;
-  block_sync<kNT>();
-  uint64_t T = ~0ull;
+  tc_tail_stamp(lv, s, 5);
+  double Tv, Hv;  // classification thresholds: Tv <= T, Hv >= H
+  if (in_smem) {
+    // T = k-th largest lower bound, H = (k+1)-th largest upper bound: only
+    // their values matter, and any Tv <= T, Hv >= H keeps the classification
+    // sound (fewer rows certain, the rest rescored exactly).  Both key arrays
+    // are sorted together (bitonic, one barrier per stage) as 32-bit keys of
+    // lo rounded down and hi rounded up, so Tv <= T and Hv >= H.
+    const int np2 = n <= 2 ? 2 : 1 << (32 - __clz(n - 1));
+    for (int i = n + threadIdx.x; i < np2; i += kNT) {
+      k32[i] = 0u;
+      k32[kTailCap + i] = 0u;
+    }
+    block_sync<kNT>();
+    block_sort2_desc_u32<kNT>(k32, k32 + kTailCap, np2);
+    Tv = k > 0 ? (double)float_of_key(k32[k - 1]) : INFINITY;  // k = 0: every row is out
+    Hv = (double)float_of_key(k32[kTailCap + k]);
+    tc_tail_stamp(lv, s, 6);
+    block_sync<kNT>();
+  } else {
+    // T = k-th largest lower bound
+    block_topk_mark<kNT>(keys, n, k, kept, sm.hist, sm.scratch);
+    uint64_t tk = ~0ull;
+    for (int i = threadIdx.x; i < n; i += kNT)
+      if (kept[i]) tk = min(tk, keys[i]);
+    for (int o = 16; o > 0; o >>= 1) tk = min(tk, (uint64_t)__shfl_xor_sync(0xffffffffu, (unsigned long long)tk, o));
+    __shared__ unsigned long long s_tk[kWarps];
+    if ((threadIdx.x & 31) == 0) s_tk[threadIdx.x >> 5] = tk;
+    block_sync<kNT>();
+    uint64_t T = ~0ull;
 #pragma unroll
-  for (int w = 0; w < kWarps; ++w) T = min(T, (uint64_t)s_tk[w]);
-  // H = (k+1)-th largest upper bound
-  for (int i = threadIdx.x; i < n; i += kNT) keys[i] = score_key(part[(int64_t)i * nsl]);
-  block_sync<kNT>();
-  block_topk_mark<kNT>(keys, n, k + 1, kept, sm.hist, sm.scratch);
-  uint64_t hk = ~0ull;
-  for (int i = threadIdx.x; i < n; i += kNT)
-    if (kept[i]) hk = min(hk, keys[i]);
-  for (int o = 16; o > 0; o >>= 1) hk = min(hk, (uint64_t)__shfl_xor_sync(0xffffffffu, (unsigned long long)hk, o));
-  if ((threadIdx.x & 31) == 0) s_tk[threadIdx.x >> 5] = hk;
-  block_sync<kNT>();
-  uint64_t H = ~0ull;
+    for (int w = 0; w < kWarps; ++w) T = min(T, (uint64_t)s_tk[w]);
+    tc_tail_stamp(lv, s, 6);
+    block_sync<kNT>();
+    // H = (k+1)-th largest upper bound
+    for (int i = threadIdx.x; i < n; i += kNT) keys[i] = score_key(part[(int64_t)i * nsl]);
+    block_sync<kNT>();
+    block_topk_mark<kNT>(keys, n, k + 1, kept, sm.hist, sm.scratch);
+    uint64_t hk = ~0ull;
+    for (int i = threadIdx.x; i < n; i += kNT)
+      if (kept[i]) hk = min(hk, keys[i]);
+    for (int o = 16; o > 0; o >>= 1) hk = min(hk, (uint64_t)__shfl_xor_sync(0xffffffffu, (unsigned long long)hk, o));
+    if ((threadIdx.x & 31) == 0) s_tk[threadIdx.x >> 5] = hk;
+    block_sync<kNT>();
+    uint64_t H = ~0ull;
 #pragma unroll
-  for (int w = 0; w < kWarps; ++w) H = min(H, (uint64_t)s_tk[w]);
+    for (int w = 0; w < kWarps; ++w) H = min(H, (uint64_t)s_tk[w]);
+    Tv = T == ~0ull ? INFINITY : double_of_key(T);
+    Hv = double_of_key(H);
+  }
+  tc_tail_stamp(lv, s, 7);
   // classify: 1 certainly in (lo > H), 2 uncertain (hi >= T), 0 out
   int n_in = 0;
   for (int i = threadIdx.x; i < n; i += kNT) {
-    const uint64_t lk = score_key(lo_v[i]);
-    const int c = lk > H ? 1 : (keys[i] >= T ? 2 : 0);
+    const double lo = lo_v[i], hi = __ldcg(part + (int64_t)i * nsl);
+    const int c = lo > Hv ? 1 : (hi >= Tv ? 2 : 0);
     cls[i] = c;
     kept[i] = c == 2;
     n_in += c == 1;
@@ -317,11 +406,13 @@ __device__ void tc_tail(const ChessState& st, const Workspace& ws, const SelPara
     meta[2] = n;
     meta[3] += n_unc;  // cumulative rows rescored (diagnostics, chess_debug_select_rescored)
   }
+  tc_tail_stamp(lv, s, 8);
   if (n_unc == 0) {
     for (int i = threadIdx.x; i < n; i += kNT) kept[i] = cls[i] == 1;
     block_sync<kNT>();
     tc_emit_level(st, ws, prm, s, lv, n, kept, sm);
   }
+  tc_tail_stamp(lv, s, 9);
 }
 
 // Tail of the rescoring launch: exact f64 scores of the uncertain rows are in
@@ -379,6 +470,10 @@ __global__ void __launch_bounds__(kTcCTA, 1) select_tc_kernel(ChessState st, Wor
   const int nsl = ws.n_slices;
   const int nkb = (int)(d.ld / 64);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (kTrace && threadIdx.x == 0 && blockIdx.x < 256) {
+    g_tc_trace[level][blockIdx.x][0] = global_ns();
+    g_tc_trace[level][blockIdx.x][3] = 0;
+  }
 
   if (warp == 0) {
     int run = 0;
@@ -525,7 +620,16 @@ __global__ void __launch_bounds__(kTcCTA, 1) select_tc_kernel(ChessState st, Wor
       block_sync<kNT>();
       if (s_last) {
         fence_acq_rel_gpu();
+        if (kTrace && threadIdx.x == 0 && s_done < 64) {
+          g_tc_tail[level][s_done][0] = global_ns();
+          g_tc_tail[level][s_done][2] = blockIdx.x;
+          g_tc_tail[level][s_done][3] = (unsigned long long)(it_end - s_prefix[s_done + 1] > 0 ? it_end - s_prefix[s_done + 1] : 0);
+        }
         tc_tail(st, ws, prm, s_done, level, s_rows[s_done], sm, s_norm);
+        if (kTrace && threadIdx.x == 0 && s_done < 64) {
+          g_tc_tail[level][s_done][1] = global_ns();
+          if (blockIdx.x < 256) g_tc_trace[level][blockIdx.x][3] += 1;
+        }
         if (threadIdx.x == 0) ws.sel_done[s_done] = 0;
         block_sync<kNT>();
       }
@@ -539,6 +643,21 @@ __global__ void __launch_bounds__(kTcCTA, 1) select_tc_kernel(ChessState st, Wor
       const TcTile p = decode(it, s);
       const int nst = stages_of(p.slice);
       if (warp < 4) {
+        // slice-0 items also gather their rows' {err, nrm} stash (mirror16)
+        // into compact per-position arrays for the tail (ws.scores and ws.keys
+        // of the slot are free during the level's scan): the loads are issued
+        // here and land while the MMAs run
+        const int r = 32 * warp + lane;  // M row = 8 * group + row in group
+        const int pos = 8 * p.g0 + r;
+        const bool valid = r < 8 * p.ng && pos < p.n;
+        const bool own_stash = valid && p.slice == 0;
+        double st_err = 0.0, st_nrm = 0.0;
+        if (own_stash) {
+          const int id = level == 0 ? pos : __ldcg(&ws.cand[((int64_t)s * 3 + level) * mr + pos]);
+          const double* sp = tc_row_stash(st, s, level, id);
+          st_err = sp[0];
+          st_nrm = sp[1];
+        }
         double acc = 0.0;
         for (int j = 0; j < nst; ++j, ++w) {
           const int b = w % kTcAcc;
@@ -551,20 +670,24 @@ __global__ void __launch_bounds__(kTcCTA, 1) select_tc_kernel(ChessState st, Wor
           if (lane == 0) mbar_arrive(&tempty[b]);
           acc = j ? __dadd_rn(acc, __dadd_rn((double)c0, (double)c1)) : __dadd_rn((double)c0, (double)c1);
         }
-        const int r = 32 * warp + lane;  // M row = 8 * group + row in group
-        const int pos = 8 * p.g0 + r;
-        if (r < 8 * p.ng && pos < p.n) {
+        if (valid) {
           const int kx = ws.anc_exp[(int64_t)s * nsl + p.slice];
           ws.part[((int64_t)s * mr + pos) * nsl + p.slice] = ldexp(acc, -kx);
+        }
+        if (own_stash) {
+          ws.scores[(int64_t)s * mr + pos] = st_err;
+          reinterpret_cast<double*>(ws.keys)[(int64_t)s * mr + pos] = st_nrm;
         }
       }
       ++contributed;
     }
     if (s >= 0) flush(s);
+    if (kTrace && threadIdx.x == 0 && blockIdx.x < 256) g_tc_trace[level][blockIdx.x][1] = global_ns();
   }
   __syncthreads();
   if (warp == kTcMmaWarp) {
     tc::fence_after();
     tc::tmem_dealloc<kTcTmemCols>(tmem);
   }
+  if (kTrace && threadIdx.x == 0 && blockIdx.x < 256) g_tc_trace[level][blockIdx.x][2] = global_ns();
 }

@@ -128,6 +128,37 @@ def test_tc_selection_equals_f64():
     torch.cuda.empty_cache()
 
 
+def test_tc_selection_large_candidate_sets():
+    """Candidate lists around and above the tail's shared-memory capacity
+    (1024): the certification thresholds come from a bitonic sort of the
+    bound keys up to 1024 candidates and from the radix top-k above it; both
+    must give the f64 selection."""
+    from helpers import index_state, load_vectors, read_selection, set_tables
+
+    rng = np.random.default_rng(33)
+    cases = [(1024, "dups", (1.0, 1.0, 0.3)), (1025, "planted", (1.0, 1.0, 0.1)),
+             (2600, "gauss", (1.0, 1.0, 0.05)), (2600, "dups", (1.0, 0.9, 0.5)), (1900, "wide", (1.0, 1.0, 0.2))]
+    for P, kind, rhos in cases:
+        cfg = SelectionConfig(pages_per_chunk=8, chunks_per_grid=8, rho_grid=rhos[0], rho_chunk=rhos[1],
+                              rho_page=rhos[2], window_pages=4, sink_pages=1)
+        dim = 2112
+        st = index_state(2, dim, P + 8, cfg, summary_dtype="f16tc")
+        hs = []
+        for slot in range(2):
+            n = P - 7 * slot
+            rows = _rows(rng, kind, n, dim)
+            load_vectors(st, slot, rows)
+            set_tables(st, slot, n + slot, cfg.sink_pages)
+            hs.append((ref.Hierarchy.from_rows(rows, cfg.pages_per_chunk, cfg.chunks_per_grid), n))
+        _select(st, cfg)
+        for slot, (h, n) in enumerate(hs):
+            sel, info = _oracle(h, cfg)
+            sem, ws, bt, prov = read_selection(st, slot)
+            np.testing.assert_array_equal(sem, sel, err_msg=f"P={n} kind={kind} rhos={rhos}")
+        del st
+    torch.cuda.empty_cache()
+
+
 def test_tc_mirror_rows_and_bounds():
     """mirror16_kernel: fp16 rows are the round-to-nearest images of the f64
     rows; the stash holds ||v - h|| and ||h|| rounded up (within 2^-19)."""

@@ -1,0 +1,9 @@
+# tc tail phase breakdown (trace build)
+mkdir -p gpurun_out/s6c
+CHESS_B200_LIB=$PWD/paper_2602_20732_b200/libchess_b200_trace.so timeout 300 python tools/select_tc_probe.py --dtypes f16tc > gpurun_out/s6c/probe_trace.json 2> gpurun_out/s6c/probe_trace.err; echo trace rc=$?
+python -c "
+import json
+d=json.loads(open('gpurun_out/s6c/probe_trace.json').read().strip().splitlines()[-1])
+print('trace us', d['us_per_pass'])
+for k,v in d['trace'].items(): print(k, json.dumps(v))
+"

@@ -79,7 +79,45 @@ def probe(dt, reps, cfg_name, batch):
                 _lib.check(lib.chess_debug_tc_read(st.ref, s, level, 0, None, None, None, m.ctypes.data, None), "read")
                 counts.append(int(m[0]))
             per_level.append(counts)
-    out = {"dtype": dt, "us_per_pass": us, "rows_scanned": rows, "rescored_rows_per_pass": per_pass, "uncertain_per_level_slot": per_level,
+    trace = {}
+    if dt == "f16tc" and hasattr(lib, "chess_debug_select_tc_trace"):
+        # trace build (CHESS_B200_LIB=.../libchess_b200_trace.so): one more pass, then
+        # the per-CTA / per-slot stamps of the three tensor-core launches and the
+        # rescoring launches (select_scan_kernel<double>, g_sel_trace / g_tail_trace)
+        call(None)
+        torch.cuda.synchronize()
+        buf = (ctypes.c_ulonglong * (3 * 256 * 4 + 3 * 64 * 12))()
+        if lib.chess_debug_select_tc_trace(buf) == 0:
+            a = np.frombuffer(buf, dtype=np.uint64).astype(np.int64)
+            ct = a[:3 * 256 * 4].reshape(3, 256, 4)[:, :148]
+            tt = a[3 * 256 * 4:].reshape(3, 64, 12)[:, :batch]
+            sb = (ctypes.c_ulonglong * (4 * 256 * 8))()
+            tb = (ctypes.c_ulonglong * (4 * 64 * 8))()
+            lib.chess_debug_select_trace(sb)
+            lib.chess_debug_select_tail_trace(tb)
+            sr = np.frombuffer(sb, dtype=np.uint64).astype(np.int64).reshape(4, 256, 8)[:, :148]
+            rt = np.frombuffer(tb, dtype=np.uint64).astype(np.int64).reshape(4, 64, 8)[:, :batch]
+            if ct[:, :, 0].max() > 0:
+                t0 = ct[0, :, 0].min()
+                us_ = lambda x: (x - t0) / 1e3
+                pct = lambda x: [round(float(np.percentile(us_(x), p)), 1) for p in (0, 50, 100)]
+                for lv in range(3):
+                    e = {"tc_entry": pct(ct[lv, :, 0]), "tc_items_done": pct(ct[lv, :, 1]),
+                         "tc_exit": pct(ct[lv, :, 2]),
+                         "tail_start": pct(tt[lv, :, 0]), "tail_end": pct(tt[lv, :, 1]),
+                         "tail_us": [round(float(x), 1) for x in np.percentile((tt[lv, :, 1] - tt[lv, :, 0]) / 1e3, (0, 50, 100))],
+                         "tail_items_left": [int(x) for x in tt[lv, :, 3]],
+                         # median per-phase time: norms, certify rows, T top-k, H top-k, classify+compact, emit
+                         "tail_phases_us": [round(float(np.median(tt[lv, :, j] - tt[lv, :, j - 1 if j > 4 else 0])) / 1e3, 2)
+                                            for j in range(4, 10)]}
+                    if sr[lv, :, 0].max() > 0:
+                        e["rescore_entry"] = pct(sr[lv, :, 0][sr[lv, :, 0] > 0])
+                        e["rescore_exit"] = pct(sr[lv, :, 4][sr[lv, :, 4] > 0])
+                        v = rt[lv, :, 4][rt[lv, :, 4] > 0]
+                        if v.size:
+                            e["rescore_tail_end"] = pct(v)
+                    trace[f"level{lv}"] = e
+    out = {"dtype": dt, "us_per_pass": us, "trace": trace, "rows_scanned": rows, "rescored_rows_per_pass": per_pass, "uncertain_per_level_slot": per_level,
            "dim": wl.shape.dim}
     print(json.dumps(out), flush=True)
     del g, dec, wl, st
