@@ -476,10 +476,10 @@ def run_gpu(args):
         results["attn_only"] = timed(dec, graphs, var_steps, args.warmup)
     del graphs
 
-    head = results["select_every_step"]
-    ms_step = head["ms"] / args.steps
+    hl = results["select_every_step"]
+    ms_step = hl["ms"] / args.steps
     value = job_batch / (ms_step / 1e3)
-    bytes_step = step_bytes(head, True)
+    bytes_step = step_bytes(hl, True)
     achieved = attn_launch_bytes / attn_launch_s / 1e9
     out = {
         "metric": "decode tokens/s (select+attn every step) at 1% KV",
@@ -502,7 +502,7 @@ def run_gpu(args):
             "kv_pool_pages": sh.n_phys,
             "kv_aliased": wl.aliased,
             "l2": "inputs larger than L2 (step reads >> 126 MB)",
-            "ws_pages_mean": head["ws_mean"],
+            "ws_pages_mean": hl["ws_mean"],
             "ws_pages_min_max_at_kernel_timing": [int(wl_now.min()), int(wl_now.max())],
             "pre_roll_tokens": pre_roll,
             "generated_pages_sealed_before_timing": 4,
@@ -545,7 +545,7 @@ def run_gpu(args):
         # kernel nodes of one captured step graph (all of them this library's
         # kernels) x steps; the formula is the fallback
         "gpu_launches": args.steps * (graph_kernels if graph_kernels else (L + 6 + (3 if head else 1))),
-        "clocks": head["clocks"],
+        "clocks": hl["clocks"],
     }
     if not args.headline_only:
         nsteps = {"select_every_step": args.steps, "dynamic": var_steps, "attn_only": var_steps}

@@ -113,6 +113,14 @@ def probe(dt, reps, cfg_name, batch):
                     if sr[lv, :, 0].max() > 0:
                         e["rescore_entry"] = pct(sr[lv, :, 0][sr[lv, :, 0] > 0])
                         e["rescore_exit"] = pct(sr[lv, :, 4][sr[lv, :, 4] > 0])
+                        e["rescore_first_row"] = pct(sr[lv, :, 2][sr[lv, :, 2] > 0])
+                        e["rescore_items_done"] = pct(sr[lv, :, 3][sr[lv, :, 3] > 0])
+                        w = rt[lv][rt[lv, :, 0] > 0]
+                        if len(w):
+                            # per-slot rescoring tail: {flush entered, counter won, reduced, top-k, done}
+                            e["rescore_tail_phases_us"] = [round(float(np.median(w[:, j] - w[:, j - 1])) / 1e3, 2)
+                                                           for j in range(1, 5)]
+                            e["rescore_tail_won"] = pct(w[:, 1])
                         v = rt[lv, :, 4][rt[lv, :, 4] > 0]
                         if v.size:
                             e["rescore_tail_end"] = pct(v)
