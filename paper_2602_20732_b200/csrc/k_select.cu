@@ -1088,10 +1088,19 @@ __global__ void __launch_bounds__(kScanCTA, 1) select_flow_kernel(ChessState st,
 // scores whole rows (lanes stride the row, fixed shuffle tree in f64) and the
 // same select_tail_topk runs between levels.
 // ---------------------------------------------------------------------------
+// Debug timeline (trace build, chess_debug_select_small_trace): per slot of
+// the last select_small_kernel launch {entry, anchor staged, then per level
+// {rows landed, scored, top-k, emitted}, exit}.
+__device__ unsigned long long g_small_trace[16][16];
+__device__ __forceinline__ void small_trace(int s, int which) {
+  if (kTrace && threadIdx.x == 0 && s < 16) g_small_trace[s][which] = global_ns();
+}
+
 template <typename T>
 __global__ void __launch_bounds__(kNT) select_small_kernel(ChessState st, Workspace ws, SelParams prm) {
   __shared__ TailSmem sm;
   const int s = blockIdx.x;
+  small_trace(s, 0);
   if (!fired(st, prm, s)) return;
   const ChessDims& d = st.d;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -1117,6 +1126,7 @@ __global__ void __launch_bounds__(kNT) select_small_kernel(ChessState st, Worksp
   const double* anc_g = st.anchor + (int64_t)s * d.ld;
   for (int j = threadIdx.x; j < d.dim; j += kNT) s_anc[j] = anc_g[j];
   block_sync<kNT>();
+  small_trace(s, 1);
   const int64_t mr = max_rows(d);
   double* sc = ws.scores + (int64_t)s * mr;
   // dot product of one summary row with the anchor by one warp: the plain
@@ -1189,26 +1199,84 @@ __global__ void __launch_bounds__(kNT) select_small_kernel(ChessState st, Worksp
     const T* base = reinterpret_cast<const T*>(sizeof(T) == 8 ? b64 : b32) + (int64_t)s * lrows * d.ld;
     for (int b0 = 0; b0 < m; b0 += batch_rows) {
       const int nr = min(batch_rows, m - b0);
-      if (threadIdx.x == 0) {
-        mbar_arrive_expect_tx(&s_rbar, (uint32_t)nr * row_bytes);
-        for (int r = 0; r < nr; ++r) {
+      if (warp == 0) {
+        // warp 0 issues the batch's bulk copies, one row per lane per round
+        if (lane == 0) mbar_arrive_expect_tx(&s_rbar, (uint32_t)nr * row_bytes);
+        __syncwarp();
+        for (int r = lane; r < nr; r += 32) {
           const int id = lv == 0 ? b0 + r : s_cand[b0 + r];
           tma_load_1d(s_rows + (size_t)r * row_bytes, base + (int64_t)id * d.ld, row_bytes, &s_rbar);
         }
       }
       mbar_wait(&s_rbar, rphase);
       rphase ^= 1u;
-      for (int r = warp; r < nr; r += kNT / 32) {
-        const double acc = dot(reinterpret_cast<const T*>(s_rows + (size_t)r * row_bytes));
+      if (b0 == 0) small_trace(s, 2 + 4 * lv);
+      // batches of more than two rows per warp: four rows per warp at once,
+      // four independent FMA chains, each in the same per-row order as dot()
+      // (so the same scores), interleaved to hide the f64 FMA latency a
+      // one-row chain exposes.  Measured on the cfg1 shape (tools/select_micro.py
+      // trace build): 32 rows 2.94 -> 2.14 us, but 4 and 16 rows slower than
+      // one chain per row (0.67 -> 1.66, 1.50 -> 2.02 us), so those keep dot().
+      if (nr <= 2 * (kNT / 32)) {
+        for (int r = warp; r < nr; r += kNT / 32) {
+          const double acc = dot(reinterpret_cast<const T*>(s_rows + (size_t)r * row_bytes));
+          if (lane == 0) {
+            sm.keys[b0 + r] = score_key(acc);
+            sc[b0 + r] = acc;
+          }
+        }
+      } else
+      for (int r0 = warp; r0 < nr; r0 += 4 * (kNT / 32)) {
+        constexpr int kR = 4;
+        double acc[kR];
+        const T* rp[kR];
+#pragma unroll
+        for (int q = 0; q < kR; ++q) {
+          const int r = min(r0 + q * (kNT / 32), nr - 1);
+          rp[q] = reinterpret_cast<const T*>(s_rows + (size_t)r * row_bytes);
+          acc[q] = 0.0;
+        }
+        for (int j0 = lane; j0 < d.dim; j0 += 32 * 8) {
+          using V = decltype(to_f(rp[0][0]));
+          V v[kR][8];
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            const int j = j0 + 32 * k;
+#pragma unroll
+            for (int q = 0; q < kR; ++q) v[q][k] = j < d.dim ? to_f(rp[q][j]) : V(0);
+          }
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            const int j = j0 + 32 * k;
+            if (j < d.dim) {
+              const double a = s_anc[j];
+#pragma unroll
+              for (int q = 0; q < kR; ++q) acc[q] = __fma_rn(a, (double)v[q][k], acc[q]);
+            }
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < kR; ++q) {
+#pragma unroll
+          for (int o = 16; o >= 1; o >>= 1) acc[q] += shfl_xor_d(acc[q], o);
+        }
         if (lane == 0) {
-          sm.keys[b0 + r] = score_key(acc);
-          sc[b0 + r] = acc;
+#pragma unroll
+          for (int q = 0; q < kR; ++q) {
+            const int r = r0 + q * (kNT / 32);
+            if (r < nr) {
+              sm.keys[b0 + r] = score_key(acc[q]);
+              sc[b0 + r] = acc[q];
+            }
+          }
         }
       }
       block_sync<kNT>();  // the staging buffer is refilled by the next batch
     }
+    small_trace(s, 3 + 4 * lv);
     const int k = (int)ceil(prm.rho[lv] * (double)m);  // selection.py:98, 103, 108
     block_topk_mark<kNT>(sm.keys, m, k, sm.kept, sm.hist, sm.scratch);
+    small_trace(s, 4 + 4 * lv);
     if (lv < 2) {
       const int kcount = block_compact<kNT>(sm.kept, m, s_plist, sm.scratch,
                                             [&](int i) { return lv == 0 ? i : s_cand[i]; });
@@ -1237,6 +1305,7 @@ __global__ void __launch_bounds__(kNT) select_small_kernel(ChessState st, Worksp
       }
     }
     block_sync<kNT>();
+    small_trace(s, 5 + 4 * lv);
   }
   __threadfence_block();
   if (prm.defer_ws) {  // the block table is being read by a concurrent decode
@@ -1244,6 +1313,7 @@ __global__ void __launch_bounds__(kNT) select_small_kernel(ChessState st, Worksp
   } else {
     block_build_ws<kNT>(st, s, sm.scratch);
   }
+  small_trace(s, 14);
 }
 
 // ---------------------------------------------------------------------------
@@ -1835,6 +1905,10 @@ extern "C" int chess_debug_select_trace(unsigned long long* host_out) {
 extern "C" int chess_debug_select_tc_trace(unsigned long long* host_out) {
   if (cudaMemcpyFromSymbol(host_out, chess::g_tc_trace, sizeof(chess::g_tc_trace)) != cudaSuccess) return 8;
   return cudaMemcpyFromSymbol(host_out + 3 * 256 * 4, chess::g_tc_tail, sizeof(chess::g_tc_tail)) == cudaSuccess ? 0 : 8;
+}
+
+extern "C" int chess_debug_select_small_trace(unsigned long long* host_out) {
+  return cudaMemcpyFromSymbol(host_out, chess::g_small_trace, sizeof(chess::g_small_trace)) == cudaSuccess ? 0 : 8;
 }
 
 extern "C" int chess_debug_select_tail_trace(unsigned long long* host_out) {

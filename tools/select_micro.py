@@ -88,6 +88,22 @@ def main():
                                        "topk": float(np.median(d[:, 3] - d[:, 2]) / 1e3),
                                        "rest": float(np.median(d[:, 4] - d[:, 3]) / 1e3),
                                        "end_vs_level_exit": float((d[:, 4].max() - tr[lv, :, 4].max()) / 1e3)}
+    sb = (ctypes.c_ulonglong * (16 * 16))()
+    lib = _lib.load()
+    if hasattr(lib, "chess_debug_select_small_trace") and lib.chess_debug_select_small_trace(sb) == 0:
+        t = np.frombuffer(sb, dtype=np.uint64).reshape(16, 16)[:b].astype(np.int64)
+        if t[:, 0].max() > 0 and t[:, 14].max() > 0:
+            # select_small_kernel (rows <= 16 KB) per-slot phases, median over slots:
+            # anchor, then per level: rows landed, scored, top-k, emitted; then the working set
+            names = ["anchor"] + [f"L{lv}_{x}" for lv in range(3) for x in ("rows", "score", "topk", "emit")] + ["ws"]
+            idx = [1] + [2 + 4 * lv + j for lv in range(3) for j in range(4)] + [14]
+            prev = t[:, 0]
+            ph = {}
+            for nme, j in zip(names, idx):
+                ph[nme] = round(float(np.median(t[:, j] - prev)) / 1e3, 2)
+                prev = t[:, j]
+            res["small_phases_us"] = ph
+            res["small_total_us"] = round(float(np.median(t[:, 14] - t[:, 0])) / 1e3, 2)
     print(json.dumps(res))
 
 
