@@ -194,10 +194,21 @@ __global__ void __launch_bounds__(kNT) entropy_kernel(ChessState st, Workspace w
   if (!s_last || warp != 0) return;
   fence_acq_rel_gpu();
   // warp 0 merges the row's split partials: lane i owns splits i and i + 32
+  // (both loaded in one round trip, merged in that order)
+  static_assert(kEntSplit <= 64, "entropy merge holds two partials per lane");
   MST c = {-INFINITY, 0.f, 0.f};
-  for (int q = lane; q < nsplit; q += 32) {
-    const double* part = ws.ent_part + ((int64_t)r * kEntSplit + q) * 3;
-    c = mst_merge(c, MST{(float)__ldcg(part), (float)__ldcg(part + 1), (float)__ldcg(part + 2)});
+  {
+    double pv[2][3];
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const int q = lane + 32 * j;
+      const double* part = ws.ent_part + ((int64_t)r * kEntSplit + q) * 3;
+#pragma unroll
+      for (int e = 0; e < 3; ++e) pv[j][e] = q < nsplit ? __ldcg(part + e) : 0.0;
+    }
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+      if (lane + 32 * j < nsplit) c = mst_merge(c, MST{(float)pv[j][0], (float)pv[j][1], (float)pv[j][2]});
   }
 #pragma unroll
   for (int o = 16; o >= 1; o >>= 1) c = mst_merge(c, mst_shfl_xor(c, o));
