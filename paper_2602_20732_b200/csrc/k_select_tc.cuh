@@ -432,6 +432,7 @@ __device__ void tc_rescore_finish(const ChessState& st, const Workspace& ws, con
   for (int i = threadIdx.x; i < n_unc; i += kNT) keys[i] = score_key(sc[i]);
   block_sync<kNT>();
   block_topk_mark<kNT>(keys, n_unc, k_rem, kept, sm.hist, sm.scratch);
+  tail_trace(lv, s, 3);
   // kept[0..n_unc) -> flags in candidate order (uncertain positions ascend)
   for (int i = threadIdx.x; i < n_unc; i += kNT) keys[i] = kept[i];
   block_sync<kNT>();
@@ -440,7 +441,9 @@ __device__ void tc_rescore_finish(const ChessState& st, const Workspace& ws, con
   for (int i = threadIdx.x; i < n_unc; i += kNT)
     if (keys[i]) kept[unc[i]] = 1;
   block_sync<kNT>();
+  tail_trace(lv, s, 5);
   tc_emit_level(st, ws, prm, s, lv, m, kept, sm);
+  tail_trace(lv, s, 6);
 }
 
 // ---------------------------------------------------------------------------

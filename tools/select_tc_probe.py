@@ -121,6 +121,9 @@ def probe(dt, reps, cfg_name, batch):
                             e["rescore_tail_phases_us"] = [round(float(np.median(w[:, j] - w[:, j - 1])) / 1e3, 2)
                                                            for j in range(1, 5)]
                             e["rescore_tail_won"] = pct(w[:, 1])
+                            # finish: reduced -> top-k -> flags scattered -> emitted -> done
+                            e["rescore_finish_us"] = [round(float(np.median(w[:, b] - w[:, a])) / 1e3, 2)
+                                                      for a, b in ((2, 3), (3, 5), (5, 6), (6, 4))]
                         v = rt[lv, :, 4][rt[lv, :, 4] > 0]
                         if v.size:
                             e["rescore_tail_end"] = pct(v)
