@@ -144,7 +144,10 @@ __device__ __forceinline__ void trace_max(int which) {
 // Cluster size cap (inbox slots = cap - 1).  Measured (profiles/r01/attn_micro/
 // sweep_cluster_cap.txt): b=1 ws16 4.3 us at 4 vs 5.3 at 8 (2-page pieces spend
 // more on merging than they save on streaming); b=4 8.6 at 4 vs 8.3 at 2.
-constexpr int kMaxCluster = 4;
+#ifndef CHESS_ATTN_CLMAX_CT
+#define CHESS_ATTN_CLMAX_CT 4
+#endif
+constexpr int kMaxCluster = CHESS_ATTN_CLMAX_CT;  // compile-time knob (build.py --define=CHESS_ATTN_CLMAX_CT=8)
 
 // XC: cluster-merge variant (piece mode with one segment per thread-block
 // cluster): the leader CTA owns an inbox for the other CTAs' piece states.
